@@ -1,0 +1,183 @@
+/*
+ * scorpio_b200 -- C ABI of the B200-native Scorpio scheduling hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  Every pointer passed to an
+ * sl_* entry point that is documented as "device" must be CUDA device memory
+ * on the current device; calls are asynchronous on `stream` and return 0 or a
+ * negative SL_ERR_* code (no exceptions cross the ABI).  Per-simulation
+ * engine failures are reported in sl_result.status (SL_SIM_*), which the
+ * Python layer maps to slosim's EngineError (simengine.py:42-43).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/slosim):
+ *   sl_run_batch        <- simengine.run(trace, SimConfig)        simengine.py:168-303
+ *                          (one call = many independent (trace, SimConfig) cells,
+ *                           as report.sweep would issue them, report.py:180-221)
+ *                          with ScorpioPolicy / plan_step          sched_scorpio.py:210-346
+ *                          and the baselines                       sched_baselines.py:49-150
+ *   sl_plan_step_batch  <- sched_scorpio.plan_step(state, ...)     sched_scorpio.py:210-316
+ *                          over many independent SchedulerStates   schedtypes.py:60-64
+ *   sl_ttft_sort_batch  <- the LDF sort inside ttft_guard          sched_scorpio.py:193
+ *   sl_guard_admit_batch<- ttft_guard walk + admission scan        sched_scorpio.py:196-294
+ *   sl_credit_select_batch <- select_batch                         sched_scorpio.py:161-180
+ *   sl_predict_batch    <- LengthPredictor.predict                 predictor.py:115-126
+ */
+#ifndef SCORPIO_B200_H
+#define SCORPIO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ------------------------------------------------------ */
+#define SL_OK 0
+#define SL_ERR_ARG (-1)
+#define SL_ERR_CUDA (-2)
+#define SL_ERR_NO_DEVICE (-3)
+
+/* ---- per-sim status word (sl_result.status) ---------------------------- */
+#define SL_SIM_OK 0
+#define SL_SIM_NO_WORK_RUNNING 1 /* EngineError simengine.py:217 */
+#define SL_SIM_NO_PROGRESS 2     /* EngineError simengine.py:220,224 */
+#define SL_SIM_LOG_OVERFLOW 4    /* decision log capacity exceeded (run continues) */
+
+/* ---- request status (core.Status, core.py:19-25) ----------------------- */
+#define SL_COMPLETED 0
+#define SL_REJECTED_TTFT 1
+#define SL_REJECTED_ADMISSION 2
+#define SL_INCOMPLETE 3
+
+/* ---- policies (SimConfig.policy, simengine.py:64-77) ------------------- */
+#define SL_POLICY_SCORPIO 0
+#define SL_POLICY_GREEDY 1
+#define SL_POLICY_SJF 2
+#define SL_POLICY_EARLY_REJECT 3
+
+/* ---- flags (ScorpioConfig sched_scorpio.py:43-60, BaselineConfig, horizon) */
+#define SL_FLAG_TTFT_GUARD 1
+#define SL_FLAG_TPOT_GUARD 2
+#define SL_FLAG_R_ONLY 4
+#define SL_FLAG_HAS_HORIZON 8
+#define SL_FLAG_PREFILL_PRIORITY 16
+
+typedef struct {
+  double alpha, beta, gamma, delta, epsilon; /* ItlParams, costmodel.py:31-47 */
+  double phi, theta, alpha_p, beta_p;        /* PrefillParams, costmodel.py:50-65 */
+} sl_cost;
+
+/* One simulation cell: a trace view under one SimConfig (simengine.py:46-61).
+ * The rate axis divides arrivals by rate_factor (workload.rescale_arrivals,
+ * workload.py:140-155); the SLO axis multiplies both thresholds by slo_scale.
+ * Both are single IEEE operations applied on device, identical to building
+ * the scaled Request objects on the host. */
+typedef struct {
+  int32_t trace;          /* index into sl_traces */
+  int32_t policy;         /* SL_POLICY_* */
+  int32_t flags;          /* SL_FLAG_* */
+  int32_t max_batch_size; /* BaselineConfig.max_batch_size */
+  double slo_scale;
+  double rate_factor;
+  double horizon; /* used iff SL_FLAG_HAS_HORIZON */
+  int32_t credit_exp;  /* E of the fixed-point credits (sl_credit_params) */
+  int32_t credit_wide; /* 1 -> 128-bit credits */
+  int64_t ws_offset;   /* first request slot of this sim in the workspace */
+  int64_t out_offset;  /* first row of this sim in sl_outcomes, -1 = none */
+  int64_t log_slot;    /* row in sl_log, -1 = no log */
+  sl_cost cost;
+} sl_sim;
+
+/* Trace table (device).  Request r of trace t lives at begin[t] + r. */
+typedef struct {
+  int32_t n_traces;
+  int32_t _pad;
+  const int64_t* begin; /* [n_traces + 1] */
+  const double* arrival;
+  const double* ttft_slo;
+  const double* tpot_slo;
+  const int32_t* prompt_len;
+  const int32_t* true_out;
+  const int32_t* predicted; /* LengthPredictor.predict output per request */
+  const int64_t* id;
+} sl_traces;
+
+/* Per-sim result row: what summarize()/goodput()/adherence() reduce to
+ * (report.py:71-134, core.py:168-179).  This is the row NCCL gathers. */
+typedef struct {
+  int32_t status;
+  int32_t _pad;
+  int64_t n_steps; /* work steps == len(EventLog.steps) */
+  int64_t n_plans; /* plan_step calls */
+  int64_t n_idle_skips;
+  int64_t request_steps; /* sum over plans of |waiting| + |running| at entry */
+  int64_t total;
+  int64_t completed;
+  int64_t compliant;
+  int64_t rejected_ttft;
+  int64_t rejected_admission;
+  int64_t incomplete;
+  int64_t ttft_violations;
+  int64_t tpot_violations;
+  double sim_end;
+  double horizon;
+  double goodput;
+  double adherence;
+  uint64_t digest; /* work-step decision digest */
+} sl_result;
+
+/* Optional per-request outcomes (RequestOutcome, core.py:59-77). */
+typedef struct {
+  int8_t* status;
+  int8_t* compliant;
+  int32_t* completion_step;
+  double* first_token_time;
+  double* completion_time;
+  double* ttft;
+  double* tpot;
+} sl_outcomes;
+
+/* Optional decision log (EventLog.steps, simengine.py:80-137), one row per
+ * sim with log_slot >= 0: step_cap steps and id_cap ids per stream per row.
+ * Ids of step k are the next n_admitted[k] / n_rejected[k] / n_batch[k]
+ * entries of the three streams; rejected ids are encoded id*2+is_admission. */
+typedef struct {
+  int64_t step_cap, id_cap;
+  double *now, *end, *prefill_s, *decode_s, *vbs, *min_slo; /* [rows*step_cap] */
+  int32_t *n_admitted, *n_rejected, *n_batch;              /* [rows*step_cap] */
+  int64_t *adm_ids, *rej_ids, *batch_ids;                  /* [rows*id_cap] */
+  int64_t* n_steps; /* [rows] steps recorded */
+} sl_log;
+
+/* Workspace bytes for `total_slots` request slots (sum over sims of trace length). */
+int64_t sl_workspace_bytes(int64_t total_slots, int32_t n_sims);
+
+/* Fixed-point credit parameters for one sim (host helper, no device work):
+ * E = min over the sim's scaled TPOT SLOs of (frexp exponent - 53); wide = 1
+ * when 2*max S >= 2^64. */
+int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_t* credit_exp,
+                     int32_t* credit_wide);
+
+/* Run n_sims independent simulations to completion.  `traces`, `outcomes`
+ * and `log` are host structs holding device pointers; `sims`, `order`,
+ * `workspace` (sl_workspace_bytes(total_slots) bytes) and `results` are
+ * device pointers.  order[] is the schedule (longest expected first); NULL =
+ * 0..n_sims-1.  outcomes / log may be NULL. */
+int sl_run_batch(const sl_traces* traces, const sl_sim* sims, const int32_t* order, int32_t n_sims,
+                 void* workspace, int64_t total_slots, sl_result* results,
+                 const sl_outcomes* outcomes, const sl_log* log, void* stream);
+
+/* Number of kernels sl_run_batch launches per call (for the gpu_launches claim). */
+int sl_run_batch_launches(void);
+
+/* ABI self-description: writes sizeof(sl_sim), sizeof(sl_result),
+ * sizeof(sl_traces), sizeof(sl_outcomes), sizeof(sl_log), sizeof(sl_cost)
+ * into out[0..5] (n >= 6).  Lets bindings verify their struct mirrors. */
+int sl_abi_layout(int64_t* out, int32_t n);
+
+/* Device properties used for grid sizing. */
+int sl_device_info(int32_t* sm_count, int32_t* l2_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,308 @@
+"""Batched device execution of many independent simulations (the sweep hot path).
+
+``BatchEngine`` owns the device buffers for one batch of simulation cells:
+the packed trace table (SoA over requests), the ``sl_sim`` cell table, the
+workspace, the per-sim result rows and optional per-request outcomes and
+decision log.  ``launch()`` is one asynchronous ``sl_run_batch`` call on the
+current torch stream; nothing on this path runs on the CPU except packing.
+
+Reference: one cell == ``slosim.simengine.run(trace, SimConfig)``
+(pkg/src/slosim/simengine.py:168-303); a batch == the cells of
+``report.sweep`` (report.py:180-221) run concurrently.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+TRACE_FIELDS = ("arrival", "ttft_slo", "tpot_slo", "prompt_len", "true_out", "predicted", "id")
+_TRACE_DTYPES = {"arrival": np.float64, "ttft_slo": np.float64, "tpot_slo": np.float64,
+                 "prompt_len": np.int32, "true_out": np.int32, "predicted": np.int32,
+                 "id": np.int64}
+
+
+@dataclass
+class TraceArrays:
+    """One trace as host SoA (request order == arrival order, trace.py semantics)."""
+
+    arrival: np.ndarray
+    ttft_slo: np.ndarray
+    tpot_slo: np.ndarray
+    prompt_len: np.ndarray
+    true_out: np.ndarray
+    predicted: np.ndarray
+    id: np.ndarray
+    category: np.ndarray | None = None
+
+    def __post_init__(self) -> None:
+        for k in TRACE_FIELDS:
+            setattr(self, k, np.ascontiguousarray(getattr(self, k), _TRACE_DTYPES[k]))
+        n = len(self.arrival)
+        if any(len(getattr(self, k)) != n for k in TRACE_FIELDS):
+            raise ValueError("trace arrays must have equal length")
+        if self.category is None:
+            self.category = np.zeros(n, np.int32)
+        validate_trace(self)
+
+    def __len__(self) -> int:
+        return len(self.arrival)
+
+
+def validate_trace(t: TraceArrays) -> None:
+    """Host-side checks that the reference raises as ValueError
+    (core.py:40-48 Request.__post_init__, simengine.py:170-178 run)."""
+    n = len(t.arrival)
+    if n == 0:
+        return
+    if np.any(t.prompt_len < 1):
+        raise ValueError("prompt_len must be >= 1")
+    if np.any(t.true_out < 1):
+        raise ValueError("true_output_len must be >= 1")
+    if np.any(~(t.ttft_slo > 0)) or np.any(~(t.tpot_slo > 0)):
+        raise ValueError("SLO thresholds must be positive")
+    if np.any(t.arrival < 0):
+        raise ValueError("arrival_time must be >= 0")
+    if np.any(np.diff(t.arrival) < 0):
+        raise ValueError("trace must be sorted by arrival time")
+    if len(np.unique(t.id)) != n:
+        raise ValueError("trace contains duplicate request ids")
+    if np.any(t.predicted < 1):
+        raise ValueError("predicted_len must be >= 1")
+
+
+@dataclass
+class CellConfig:
+    """The SimConfig of one cell (simengine.py:46-61), flattened."""
+
+    policy: str = "scorpio"
+    itl: tuple = (1e-6, 1e-3, 1e-5, 5e-3, 1.1)  # alpha, beta, gamma, delta, epsilon
+    prefill: tuple = (0.004, 128.0, 2e-5, 1.5e-3)  # phi, theta, alpha_p, beta_p
+    ttft_guard: bool = True
+    tpot_guard: bool = True
+    admission_min: str = "r_prime"
+    max_batch_size: int = 256
+    prefill_priority: bool = False
+    horizon: float | None = None
+
+    def flags(self) -> int:
+        f = 0
+        if self.ttft_guard:
+            f |= N.FLAG_TTFT_GUARD
+        if self.tpot_guard:
+            f |= N.FLAG_TPOT_GUARD
+        if self.admission_min == "r_only":
+            f |= N.FLAG_R_ONLY
+        elif self.admission_min != "r_prime":
+            raise ValueError(f"unknown admission_min {self.admission_min!r}")
+        if self.horizon is not None:
+            if not self.horizon > 0:
+                raise ValueError("horizon must be positive when finite")
+            f |= N.FLAG_HAS_HORIZON
+        if self.prefill_priority:
+            f |= N.FLAG_PREFILL_PRIORITY
+        return f
+
+
+@dataclass
+class Cell:
+    """One simulation: trace index, config, and the sweep axes."""
+
+    trace: int
+    config: CellConfig = field(default_factory=CellConfig)
+    slo_scale: float = 1.0
+    rate_factor: float = 1.0
+
+
+def pack_cells(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = False,
+               log_cells: list[int] | None = None) -> np.ndarray:
+    """Build the sl_sim table (host); workspace/outcome offsets by prefix sum."""
+    sims = np.zeros(len(cells), N.SIM_DTYPE)
+    uniq = [np.unique(t.tpot_slo) for t in traces]
+    ws = 0
+    log_rows = {c: r for r, c in enumerate(log_cells or [])}
+    for k, c in enumerate(cells):
+        t = traces[c.trace]
+        cfg = c.config
+        if cfg.policy not in N.POLICY:
+            raise ValueError(f"unknown policy {cfg.policy!r}")
+        if not c.slo_scale > 0 or not c.rate_factor > 0:
+            raise ValueError("slo_scale and rate_factor must be positive")
+        a, b, g, d, e = cfg.itl
+        if e < 1.0:
+            raise ValueError("epsilon must be >= 1.0")
+        phi, th, ap, bp = cfg.prefill
+        if phi <= 0 or th < 0 or ap * th + bp < 0:
+            raise ValueError("invalid PrefillParams")
+        if cfg.max_batch_size < 1:
+            raise ValueError("max_batch_size must be >= 1")
+        E, wide = N.credit_params(uniq[c.trace], c.slo_scale)
+        s = sims[k]
+        s["trace"] = c.trace
+        s["policy"] = N.POLICY[cfg.policy]
+        s["flags"] = cfg.flags()
+        s["max_batch_size"] = cfg.max_batch_size
+        s["slo_scale"] = c.slo_scale
+        s["rate_factor"] = c.rate_factor
+        s["horizon"] = cfg.horizon if cfg.horizon is not None else 0.0
+        s["credit_exp"] = E
+        s["credit_wide"] = wide
+        s["ws_offset"] = ws
+        s["out_offset"] = ws if outcomes else -1
+        s["log_slot"] = log_rows.get(k, -1)
+        for name, v in zip(N.COST_FIELDS, (a, b, g, d, e, phi, th, ap, bp)):
+            s[name] = v
+        ws += len(t)
+    return sims
+
+
+class BatchEngine:
+    """Device buffers + launch for one batch of cells (reusable across launches)."""
+
+    def __init__(self, traces: list[TraceArrays], cells: list[Cell] | np.ndarray,
+                 outcomes: bool = False, log_cells: list[int] | None = None,
+                 log_steps: int = 0, log_ids: int = 0, order: np.ndarray | None = None,
+                 device=None):
+        torch = N.require_cuda()
+        self.torch = torch
+        self.device = torch.device(device if device is not None else "cuda")
+        if isinstance(cells, np.ndarray):
+            sims = cells
+        else:
+            sims = pack_cells(traces, cells, outcomes, log_cells)
+        self.n_sims = len(sims)
+        self.sims_host = sims
+        lens = np.array([len(t) for t in traces], np.int64)
+        begin = np.zeros(len(traces) + 1, np.int64)
+        np.cumsum(lens, out=begin[1:])
+        self.trace_begin = begin
+        dev = self.device
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+        self._tr = {k: up(np.concatenate([getattr(t, k) for t in traces]) if traces else
+                          np.zeros(0, _TRACE_DTYPES[k])) for k in TRACE_FIELDS}
+        self._tr["begin"] = up(begin)
+        self._sims = up(sims.view(np.uint8))
+        self.total_slots = int(sum(lens[s["trace"]] for s in sims)) if len(sims) else 0
+        wsb = N.lib().sl_workspace_bytes(self.total_slots, self.n_sims)
+        self._ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        self._res = torch.zeros(self.n_sims * N.RESULT_DTYPE.itemsize, dtype=torch.uint8,
+                                device=dev)
+        if order is None:
+            order = default_order(traces, sims)
+        self._order = up(np.ascontiguousarray(order, np.int32))
+        self.st = N.SlTraces(len(traces), 0, *[self._tr[k].data_ptr() for k in (
+            "begin", "arrival", "ttft_slo", "tpot_slo", "prompt_len", "true_out", "predicted",
+            "id")])
+        self.has_outcomes = bool(outcomes)
+        self.oc = None
+        if outcomes:
+            m = max(self.total_slots, 1)
+            self._out = {
+                "status": torch.empty(m, dtype=torch.int8, device=dev),
+                "compliant": torch.empty(m, dtype=torch.int8, device=dev),
+                "completion_step": torch.empty(m, dtype=torch.int32, device=dev),
+                "first_token_time": torch.empty(m, dtype=torch.float64, device=dev),
+                "completion_time": torch.empty(m, dtype=torch.float64, device=dev),
+                "ttft": torch.empty(m, dtype=torch.float64, device=dev),
+                "tpot": torch.empty(m, dtype=torch.float64, device=dev),
+            }
+            self.oc = N.SlOutcomes(*[self._out[k].data_ptr() for k in (
+                "status", "compliant", "completion_step", "first_token_time", "completion_time",
+                "ttft", "tpot")])
+        self.lg = None
+        rows = int((sims["log_slot"] >= 0).sum()) if len(sims) else 0
+        if rows and log_steps > 0:
+            sc, ic = int(log_steps), int(max(log_ids, 1))
+            f64 = dict(dtype=torch.float64, device=dev)
+            i32 = dict(dtype=torch.int32, device=dev)
+            i64 = dict(dtype=torch.int64, device=dev)
+            self._log = {k: torch.zeros(rows * sc, **f64) for k in (
+                "now", "end", "prefill_s", "decode_s", "vbs", "min_slo")}
+            for k in ("n_admitted", "n_rejected", "n_batch"):
+                self._log[k] = torch.zeros(rows * sc, **i32)
+            for k in ("adm_ids", "rej_ids", "batch_ids"):
+                self._log[k] = torch.zeros(rows * ic, **i64)
+            self._log["n_steps"] = torch.zeros(rows, **i64)
+            self.log_shape = (rows, sc, ic)
+            self.lg = N.SlLog(sc, ic, *[self._log[k].data_ptr() for k in (
+                "now", "end", "prefill_s", "decode_s", "vbs", "min_slo", "n_admitted",
+                "n_rejected", "n_batch", "adm_ids", "rej_ids", "batch_ids", "n_steps")])
+
+    def launch(self, stream=None) -> None:
+        """One sl_run_batch on `stream` (default: torch's current stream)."""
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = N.lib().sl_run_batch(
+            C.byref(self.st), self._sims.data_ptr(), self._order.data_ptr(), self.n_sims,
+            self._ws.data_ptr(), self.total_slots, self._res.data_ptr(),
+            C.byref(self.oc) if self.oc is not None else None,
+            C.byref(self.lg) if self.lg is not None else None, s.cuda_stream)
+        if rc != 0:
+            raise RuntimeError(f"sl_run_batch failed with code {rc}")
+
+    def results(self) -> np.ndarray:
+        """Per-sim result rows (host, sl_result dtype); synchronizes."""
+        return self._res.cpu().numpy().view(N.RESULT_DTYPE).copy()
+
+    def results_device(self):
+        return self._res
+
+    def outcomes(self) -> dict[str, np.ndarray]:
+        if not self.has_outcomes:
+            raise RuntimeError("engine built without outcomes")
+        return {k: v[: self.total_slots].cpu().numpy() for k, v in self._out.items()}
+
+    def sim_outcomes(self, k: int, all_out: dict | None = None) -> dict[str, np.ndarray]:
+        """Outcome arrays of cell k (slices of outcomes())."""
+        all_out = all_out if all_out is not None else self.outcomes()
+        s = self.sims_host[k]
+        b = int(s["out_offset"])
+        n = int(self.trace_begin[s["trace"] + 1] - self.trace_begin[s["trace"]])
+        return {f: v[b:b + n] for f, v in all_out.items()}
+
+    def log(self, k: int) -> dict:
+        """Decision log of cell k (must have a log slot)."""
+        row = int(self.sims_host[k]["log_slot"])
+        if row < 0 or self.lg is None:
+            raise RuntimeError("cell has no log slot")
+        rows, sc, ic = self.log_shape
+        ns = int(self._log["n_steps"][row].item())
+        out = {f: self._log[f][row * sc: row * sc + ns].cpu().numpy() for f in (
+            "now", "end", "prefill_s", "decode_s", "vbs", "min_slo", "n_admitted", "n_rejected",
+            "n_batch")}
+        na, nr, nb = (int(out[f].sum()) for f in ("n_admitted", "n_rejected", "n_batch"))
+        out["adm_ids"] = self._log["adm_ids"][row * ic: row * ic + na].cpu().numpy()
+        out["rej_ids"] = self._log["rej_ids"][row * ic: row * ic + nr].cpu().numpy()
+        out["batch_ids"] = self._log["batch_ids"][row * ic: row * ic + nb].cpu().numpy()
+        return out
+
+
+def default_order(traces: list[TraceArrays], sims: np.ndarray) -> np.ndarray:
+    """Longest-expected-first schedule: sims with the lowest arrival rate have the
+    longest step chains, so they start first."""
+    if len(sims) == 0:
+        return np.zeros(0, np.int32)
+    rate = np.empty(len(sims))
+    for k, s in enumerate(sims):
+        t = traces[s["trace"]]
+        span = float(t.arrival[-1]) / float(s["rate_factor"]) if len(t) else 0.0
+        rate[k] = len(t) / span if span > 0 else np.inf
+    # low rate first; ties by larger trace first
+    key = np.lexsort((-np.array([len(traces[s["trace"]]) for s in sims]), rate))
+    return key.astype(np.int32)
+
+
+def run_batch(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = False,
+              log_cells: list[int] | None = None, log_steps: int = 0, log_ids: int = 0):
+    """Convenience: build, launch, and return (results, engine)."""
+    eng = BatchEngine(traces, cells, outcomes=outcomes, log_cells=log_cells,
+                      log_steps=log_steps, log_ids=log_ids)
+    eng.launch()
+    return eng.results(), eng

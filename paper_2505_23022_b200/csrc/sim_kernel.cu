@@ -1,0 +1,913 @@
+// Persistent warp-per-simulation kernel: the whole slosim discrete-event loop
+// (simengine.run, simengine.py:168-303) with the scorpio policy
+// (sched_scorpio.plan_step, sched_scorpio.py:210-316) or a baseline
+// (sched_baselines.py:49-150), for thousands of independent simulations.
+//
+// Mapping:
+//  * one warp owns one simulation at a time and pulls the next one from a
+//    device work counter over a host-ordered (longest-first) schedule;
+//  * per-request arrival-time constants live in a 64-byte WRec, written once
+//    when the request becomes visible; the waiting queue is an int32 index
+//    list kept in LDF order by warp-parallel rank+shift insertion;
+//  * the running set is a positional SoA (32-byte RRec per entry, admission
+//    order) so credit updates, emits and retire compaction are coalesced
+//    lane-parallel passes; batch compaction = ballot + popc;
+//  * the order-dependent fp64 chains (TTFT prefix walk, Neumaier aggregates,
+//    greedy admission scan) run warp-uniformly over register-staged chunks
+//    (one chunk load per 32 items, values broadcast with shuffles) so every
+//    lane holds the same state and no lane diverges.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "scorpio_b200.h"
+#include "sl_device.cuh"
+
+using namespace sl;
+
+namespace {
+
+struct __align__(16) WRec {  // per request, written at arrival (WaitingItem + Request fields)
+  double arr;       // arrival_time / rate_factor
+  double ttft;      // ttft_slo * slo_scale
+  double prefill;   // prefill_time(prompt_len), costmodel.py:132-138
+  double tpot;      // tpot_slo * slo_scale
+  double inv;       // 1.0 / tpot
+  double deadline;  // arr + ttft, core.py:50-53
+  uint64_t S;       // fixed-point tpot (low 64 bits)
+  int32_t prompt;
+  int32_t pred_solo;  // predicted_len | solo_ok << 31
+};
+static_assert(sizeof(WRec) == 64, "WRec layout");
+
+struct __align__(16) RRec {  // per running entry, positional (RunningEntry)
+  uint64_t N;   // credit * slo / 2^E (low 64 bits)
+  uint64_t S;   // slo / 2^E (low 64 bits)
+  double inv;   // 1.0 / tpot
+  int32_t cur_len;  // prompt_len + tokens_generated
+  int32_t rem;      // true_output_len - tokens_generated
+};
+static_assert(sizeof(RRec) == 32, "RRec layout");
+
+struct Workspace {  // SoA regions over all request slots
+  int* counter;
+  int32_t* wl;       // waiting list (request index), per sim [n]
+  int32_t* rl;       // running list (request index), per sim [n]
+  WRec* wr;          // per request
+  RRec* rr;          // per running position
+  uint64_t* wShi;    // wide credits: S high word per request
+  uint64_t* rNhi;    // wide credits: per running position
+  uint64_t* rShi;
+  double* first_emit;  // per request
+};
+
+__host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+__host__ __device__ inline Workspace carve(void* base, int64_t slots) {
+  Workspace w;
+  char* p = (char*)base;
+  int64_t off = 0;
+  w.counter = (int*)(p + off);
+  off += 256;
+  w.wl = (int32_t*)(p + off);
+  off = align256(off + slots * 4);
+  w.rl = (int32_t*)(p + off);
+  off = align256(off + slots * 4);
+  w.wr = (WRec*)(p + off);
+  off = align256(off + slots * 64);
+  w.rr = (RRec*)(p + off);
+  off = align256(off + slots * 32);
+  w.wShi = (uint64_t*)(p + off);
+  off = align256(off + slots * 8);
+  w.rNhi = (uint64_t*)(p + off);
+  off = align256(off + slots * 8);
+  w.rShi = (uint64_t*)(p + off);
+  off = align256(off + slots * 8);
+  w.first_emit = (double*)(p + off);
+  return w;
+}
+
+__host__ __device__ inline int64_t workspace_bytes(int64_t slots) {
+  return 256 + 8 * 256 + align256(slots * 4) * 2 + align256(slots * 64) + align256(slots * 32) +
+         align256(slots * 8) * 4;
+}
+
+struct KArgs {
+  sl_traces tr;
+  const sl_sim* sims;
+  const int32_t* order;
+  int32_t n_sims;
+  int64_t slots;
+  void* ws_base;
+  sl_result* results;
+  sl_outcomes out;
+  int has_out;
+  sl_log log;
+  int has_log;
+};
+
+// Per-sim view, warp-uniform.
+struct Sim {
+  // trace
+  const double* arrival;
+  const double* ttft_b;
+  const double* tpot_b;
+  const int32_t* prompt;
+  const int32_t* true_out;
+  const int32_t* predicted;
+  const int64_t* id;
+  int64_t n;
+  // params
+  sl_cost cost;
+  double scale, factor, horizon, pow2E;
+  int policy, flags, cap, E;
+  // workspace slices
+  int32_t* wl;
+  int32_t* rl;
+  WRec* wr;
+  RRec* rr;
+  uint64_t* wShi;
+  uint64_t* rNhi;
+  uint64_t* rShi;
+  double* first_emit;
+  // outputs
+  int64_t out_off;
+  int64_t log_row;
+};
+
+__device__ __forceinline__ bool key_less_ldf(const Sim& s, double da, double aa, int ia, double db,
+                                             double ab, int ib) {
+  // sort_key = (deadline, arrival_time, id), schedtypes.py:28-32
+  if (da != db) return da < db;
+  if (aa != ab) return aa < ab;
+  return s.id[ia] < s.id[ib];
+}
+
+__device__ __forceinline__ bool key_less_sjf(const Sim& s, int32_t pa, double aa, int ia,
+                                             int32_t pb, double ab, int ib) {
+  // sched_baselines.py:138-142 key (predicted_len, arrival_time, id)
+  if (pa != pb) return pa < pb;
+  if (aa != ab) return aa < ab;
+  return s.id[ia] < s.id[ib];
+}
+
+// Insert request `idx` into the sorted waiting list at its rank (keys are
+// unique, so rank == bisect position).  Warp-cooperative: O(W/32) compares
+// and a top-down chunked shift.
+__device__ void insert_sorted(const Sim& s, int& W, int idx, bool sjf, int lane) {
+  const WRec& me = s.wr[idx];
+  double dk = me.deadline, ak = me.arr;
+  int32_t pk = me.pred_solo & 0x7fffffff;
+  int pos = 0;
+  for (int c0 = 0; c0 < W; c0 += 32) {
+    int j = c0 + lane;
+    bool lt = false;
+    if (j < W) {
+      int o = s.wl[j];
+      const WRec& r = s.wr[o];
+      lt = sjf ? key_less_sjf(s, r.pred_solo & 0x7fffffff, r.arr, o, pk, ak, idx)
+               : key_less_ldf(s, r.deadline, r.arr, o, dk, ak, idx);
+    }
+    pos += __popc(__ballot_sync(SL_FULL, lt));
+  }
+  // shift [pos, W) up by one, highest chunk first
+  int tail = W - pos;
+  for (int c = (tail - 1) / 32; c >= 0 && tail > 0; --c) {
+    int j = pos + c * 32 + lane;
+    int v = 0;
+    bool ok = j < W;
+    if (ok) v = s.wl[j];
+    __syncwarp();
+    if (ok) s.wl[j + 1] = v;
+    __syncwarp();
+  }
+  if (lane == 0) s.wl[pos] = idx;
+  __syncwarp();
+  W += 1;
+}
+
+// Per-lane accumulators folded into the result row at the end.
+struct Acc {
+  uint64_t dig;       // committed digest partial
+  uint64_t dig_rej;   // pending (rejections of the current plan)
+  int64_t completed, compliant, rej_ttft, rej_adm, ttft_viol, tpot_viol;
+  int64_t prej_ttft, prej_adm;  // (counted immediately; outcomes are final)
+};
+
+// TTFT prefix walk over wl[0, W) in list order (ttft_guard :196-205 /
+// early_reject sched_baselines.py:95-103).  Rejected -> REJECTED_TTFT.
+__device__ void ttft_walk(const Sim& s, const KArgs& a, bool has_out, int& W, int& nrej,
+                          double now, int64_t step, Acc& acc, int lane, int64_t log_rej_base,
+                          int64_t log_cap) {
+  double prefix = 0.0;
+  int kept = 0;
+  for (int c0 = 0; c0 < W; c0 += 32) {
+    int j = c0 + lane;
+    bool valid = j < W;
+    int idx = 0;
+    double e = 0.0, pf = 0.0, tt = 0.0;
+    if (valid) {
+      idx = s.wl[j];
+      const WRec& r = s.wr[idx];
+      e = fsub_(now, r.arr);
+      pf = r.prefill;
+      tt = r.ttft;
+    }
+    int cnt = min(32, W - c0);
+    unsigned rej = 0;
+    for (int t = 0; t < cnt; ++t) {
+      double et = bcast(e, t), pt = bcast(pf, t), tl = bcast(tt, t);
+      double est = fadd_(fadd_(et, prefix), pt);
+      if (est > tl)
+        rej |= 1u << t;
+      else
+        prefix = fadd_(prefix, pt);
+    }
+    bool r_ = valid && ((rej >> lane) & 1u);
+    bool keep = valid && !r_;
+    unsigned km = __ballot_sync(SL_FULL, keep);
+    __syncwarp();
+    if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
+    if (r_) {
+      int pos = nrej + __popc(rej & lanemask_lt());
+      int64_t rid = s.id[idx];
+      acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u);
+      acc.rej_ttft++;
+      if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_TTFT;
+      if (log_rej_base >= 0 && pos < log_cap) a.log.rej_ids[log_rej_base + pos] = rid * 2;
+    }
+    __syncwarp();
+    kept += __popc(km);
+    nrej += __popc(rej);
+  }
+  W = kept;
+}
+
+// Append waiting items wl[0, take) to the running list in order (admit-all /
+// admit_fcfs) and shift the waiting list down.  Returns the Neumaier prefill sum.
+template <bool WIDE>
+__device__ void admit_prefix(const Sim& s, const KArgs& a, int& W, int& R, int take, int& nadm,
+                             PySum& P, int64_t step, Acc& acc, int lane, int64_t log_adm_base,
+                             int64_t log_cap) {
+  for (int c0 = 0; c0 < take; c0 += 32) {
+    int j = c0 + lane;
+    bool valid = j < take;
+    double pf = 0.0;
+    if (valid) {
+      int idx = s.wl[j];
+      const WRec& w = s.wr[idx];
+      pf = w.prefill;
+      RRec r;
+      r.N = 0;
+      r.S = w.S;
+      r.inv = w.inv;
+      r.cur_len = w.prompt;
+      r.rem = s.true_out[idx];
+      s.rr[R + j] = r;
+      s.rl[R + j] = idx;
+      if constexpr (WIDE) {
+        s.rNhi[R + j] = 0;
+        s.rShi[R + j] = s.wShi[idx];
+      }
+      int64_t rid = s.id[idx];
+      acc.dig += digest_item((uint64_t)step, 0, (uint32_t)(nadm + j), (uint64_t)rid);
+      if (log_adm_base >= 0 && nadm + j < log_cap) a.log.adm_ids[log_adm_base + nadm + j] = rid;
+    }
+    int cnt = min(32, take - c0);
+    for (int t = 0; t < cnt; ++t) ps_add(P, bcast(pf, t));
+  }
+  __syncwarp();
+  // shift remaining waiting items down by `take`
+  int rest = W - take;
+  for (int c0 = 0; c0 < rest; c0 += 32) {
+    int j = c0 + lane;
+    int v = 0;
+    if (j < rest) v = s.wl[take + j];
+    __syncwarp();
+    if (j < rest) s.wl[j] = v;
+    __syncwarp();
+  }
+  R += take;
+  nadm += take;
+  W = rest;
+}
+
+template <bool WIDE>
+__device__ __forceinline__ cred_t<WIDE> load_S(const Sim& s, int j) {
+  if constexpr (WIDE)
+    return ((unsigned __int128)s.rShi[j] << 64) | s.rr[j].S;
+  else
+    return s.rr[j].S;
+}
+
+// min over running S in [0, R) -> fixed value (warp-uniform)
+template <bool WIDE>
+__device__ cred_t<WIDE> running_min_S(const Sim& s, int R, int lane) {
+  cred_t<WIDE> m = ~cred_t<WIDE>(0);
+  for (int j = lane; j < R; j += 32) {
+    cred_t<WIDE> v = load_S<WIDE>(s, j);
+    m = v < m ? v : m;
+  }
+  return warp_min_cred<WIDE>(m);
+}
+
+template <bool WIDE>
+__device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_index, int lane) {
+  const int64_t n = s.n;
+  const sl_cost& C = s.cost;
+  const bool scorpio = s.policy == SL_POLICY_SCORPIO;
+  const bool ttft_guard = (s.flags & SL_FLAG_TTFT_GUARD) != 0;
+  const bool tpot_guard = (s.flags & SL_FLAG_TPOT_GUARD) != 0;
+  const bool r_only = (s.flags & SL_FLAG_R_ONLY) != 0;
+  const bool has_h = (s.flags & SL_FLAG_HAS_HORIZON) != 0;
+  const bool sorted_ldf = scorpio && ttft_guard;
+  const bool sjf = s.policy == SL_POLICY_SJF;
+
+  if (has_out) {
+    for (int64_t i = lane; i < n; i += 32) {
+      int64_t o = s.out_off + i;
+      a.out.status[o] = SL_INCOMPLETE;
+      a.out.compliant[o] = 0;
+      a.out.completion_step[o] = -1;
+      a.out.first_token_time[o] = __longlong_as_double(0x7ff8000000000000LL);
+      a.out.completion_time[o] = __longlong_as_double(0x7ff8000000000000LL);
+      a.out.ttft[o] = __longlong_as_double(0x7ff8000000000000LL);
+      a.out.tpot[o] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+  }
+  const bool logging = a.has_log && s.log_row >= 0;
+  int64_t lg_step0 = logging ? s.log_row * a.log.step_cap : 0;
+  int64_t lg_id0 = logging ? s.log_row * a.log.id_cap : 0;
+  int64_t cur_adm = 0, cur_rej = 0, cur_batch = 0;  // log stream cursors
+  bool log_over = false;
+
+  Acc acc;
+  memset(&acc, 0, sizeof(acc));
+  double now = 0.0;
+  int64_t next = 0;
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  double next_t = n > 0 ? fdiv_(s.arrival[0], s.factor) : kInf;
+  int W = 0, R = 0;
+  int64_t step = 0, n_plans = 0, n_idle = 0, req_steps = 0;
+  int status = SL_SIM_OK;
+
+  for (;;) {
+    // ---- arrivals become visible at step boundaries (simengine.py:186-188)
+    while (next < n && next_t <= now) {
+      int64_t i = next + lane;
+      double ai = (i < n) ? fdiv_(s.arrival[i], s.factor) : kInf;
+      bool c = ai <= now;
+      unsigned m = __ballot_sync(SL_FULL, c);
+      int k = __popc(m);  // arrivals are sorted: m is a lane prefix
+      if (c) {
+        WRec w;
+        w.arr = ai;
+        w.ttft = fmul_(s.ttft_b[i], s.scale);
+        w.tpot = fmul_(s.tpot_b[i], s.scale);
+        w.prompt = s.prompt[i];
+        int32_t pred = s.predicted[i];
+        w.prefill = prefill_time(C, w.prompt);
+        w.inv = fdiv_(1.0, w.tpot);
+        w.deadline = fadd_(w.arr, w.ttft);
+        cred_t<WIDE> S = slo_fixed<WIDE>(w.tpot, s.E);
+        w.S = (uint64_t)S;
+        if constexpr (WIDE) s.wShi[i] = (uint64_t)(S >> 64);
+        bool solo = solo_ok(C, w.tpot, w.inv, w.prompt, pred);
+        w.pred_solo = pred | (solo ? (int32_t)0x80000000 : 0);
+        s.wr[i] = w;
+      }
+      __syncwarp();
+      if (sorted_ldf || sjf) {
+        for (int t = 0; t < k; ++t) insert_sorted(s, W, (int)(next + t), sjf, lane);
+      } else {
+        if (c) s.wl[W + lane] = (int32_t)i;
+        __syncwarp();
+        W += k;
+      }
+      next += k;
+      next_t = next < n ? fdiv_(s.arrival[next], s.factor) : kInf;
+    }
+
+    if (has_h && now >= s.horizon) break;  // simengine.py:190-191
+
+    // ---- plan (policy.plan)
+    n_plans++;
+    req_steps += W + R;
+    const int R0 = R;
+    int nadm = 0, nrej = 0, nbatch = 0;
+    PySum P;
+    ps_init(P);
+    int64_t blen = 0;  // per-lane partial of sum(current_len) over the batch
+    acc.dig_rej = 0;
+    int64_t lg_adm = (logging && !log_over) ? lg_id0 + cur_adm : -1;
+    int64_t lg_rej = (logging && !log_over) ? lg_id0 + cur_rej : -1;
+    int64_t lg_bat = (logging && !log_over) ? lg_id0 + cur_batch : -1;
+    // clamp stream bases so that positions beyond id_cap are dropped (overflow flagged below)
+    int64_t cap_adm = logging ? a.log.id_cap - cur_adm : 0;
+    int64_t cap_rej = logging ? a.log.id_cap - cur_rej : 0;
+    int64_t cap_bat = logging ? a.log.id_cap - cur_batch : 0;
+
+    if (scorpio) {
+      if (ttft_guard && W > 0)
+        ttft_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej);
+      if (tpot_guard) {
+        if (W > 0) {
+          // _running_aggregates (sched_scorpio.py:117-124)
+          int64_t n_run = R;
+          int64_t lens = 0;
+          for (int j = lane; j < R; j += 32) lens += s.rr[j].cur_len;
+          lens = warp_sum_i64(lens);
+          cred_t<WIDE> Smin = running_min_S<WIDE>(s, R, lane);
+          bool has_min = R > 0;
+          double min_d = has_min ? fixed_to_double<WIDE>(Smin, s.pow2E) : 0.0;
+          PySum ps;
+          ps_init(ps);
+          for (int c0 = 0; c0 < R; c0 += 32) {
+            int j = c0 + lane;
+            double x = j < R ? s.rr[j].inv : 0.0;
+            int cnt = min(32, R - c0);
+            for (int t = 0; t < cnt; ++t) ps_add(ps, bcast(x, t));
+          }
+          double inv = ps_result(ps);
+          // admission scan in queue order (sched_scorpio.py:237-294)
+          int kept = 0;
+          for (int c0 = 0; c0 < W; c0 += 32) {
+            int j = c0 + lane;
+            bool valid = j < W;
+            int idx = 0;
+            double tp = 0.0, ic = 0.0, pf = 0.0;
+            int32_t ln = 0, ps_ = 0;
+            cred_t<WIDE> Sc = 0;
+            if (valid) {
+              idx = s.wl[j];
+              const WRec& w = s.wr[idx];
+              tp = w.tpot;
+              ic = w.inv;
+              pf = w.prefill;
+              ln = w.prompt;
+              ps_ = w.pred_solo;
+              if constexpr (WIDE)
+                Sc = ((unsigned __int128)s.wShi[idx] << 64) | w.S;
+              else
+                Sc = w.S;
+            }
+            int cnt = min(32, W - c0);
+            unsigned adm = 0;
+            for (int t = 0; t < cnt; ++t) {
+              double cand = bcast(tp, t);
+              double icand = bcast(ic, t);
+              int32_t clen = bcast(ln, t);
+              int32_t cpred = bcast(ps_, t) & 0x7fffffff;
+              bool lt = !has_min || cand < min_d;
+              double minp = lt ? cand : min_d;
+              double V = fmul_(minp, fadd_(inv, icand));
+              double L = fdiv_((double)(lens + clen), (double)(n_run + 1));
+              double est = tpot_estimate(C, V, L, cpred);
+              double thr = (r_only && has_min) ? min_d : minp;
+              if (est <= thr) {
+                adm |= 1u << t;
+                n_run += 1;
+                inv = fadd_(inv, icand);  // plain float add, :275
+                lens += clen;
+                if (lt) min_d = cand;
+                has_min = true;
+                ps_add(P, bcast(pf, t));
+              }
+            }
+            bool is_adm = valid && ((adm >> lane) & 1u);
+            bool solo = (ps_ & (int32_t)0x80000000) != 0;
+            bool keep = valid && !is_adm && solo;
+            bool rj = valid && !is_adm && !solo;
+            unsigned km = __ballot_sync(SL_FULL, keep);
+            unsigned rm = __ballot_sync(SL_FULL, rj);
+            __syncwarp();
+            if (is_adm) {
+              int q = __popc(adm & lanemask_lt());
+              RRec r;
+              r.N = 0;
+              r.S = (uint64_t)Sc;
+              r.inv = ic;
+              r.cur_len = ln;
+              r.rem = s.true_out[idx];
+              s.rr[R + q] = r;
+              s.rl[R + q] = idx;
+              if constexpr (WIDE) {
+                s.rNhi[R + q] = 0;
+                s.rShi[R + q] = (uint64_t)(Sc >> 64);
+              }
+              int64_t rid = s.id[idx];
+              acc.dig += digest_item((uint64_t)step, 0, (uint32_t)(nadm + q), (uint64_t)rid);
+              if (lg_adm >= 0 && nadm + q < cap_adm) a.log.adm_ids[lg_adm + nadm + q] = rid;
+            }
+            if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
+            if (rj) {
+              int pos = nrej + __popc(rm & lanemask_lt());
+              int64_t rid = s.id[idx];
+              acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u + 1u);
+              acc.rej_adm++;
+              if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_ADMISSION;
+              if (lg_rej >= 0 && pos < cap_rej) a.log.rej_ids[lg_rej + pos] = rid * 2 + 1;
+            }
+            __syncwarp();
+            int na = __popc(adm);
+            R += na;
+            nadm += na;
+            kept += __popc(km);
+            nrej += __popc(rm);
+          }
+          W = kept;
+        }
+      } else {
+        admit_prefix<WIDE>(s, a, W, R, W, nadm, P, step, acc, lane, lg_adm, cap_adm);
+      }
+    } else {
+      if (s.policy == SL_POLICY_EARLY_REJECT && W > 0)
+        ttft_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej);
+      int room = s.cap - R;
+      int take = room > 0 ? min(room, W) : 0;
+      if (take > 0)
+        admit_prefix<WIDE>(s, a, W, R, take, nadm, P, step, acc, lane, lg_adm, cap_adm);
+    }
+
+    // ---- decode batch
+    cred_t<WIDE> MIN = 0;
+    bool need_min = scorpio && (tpot_guard || logging);
+    if (need_min && R > 0) MIN = running_min_S<WIDE>(s, R, lane);
+    const bool credit = scorpio && tpot_guard;
+    const bool decode_all = !credit && !(s.policy != SL_POLICY_SCORPIO &&
+                                         (s.flags & SL_FLAG_PREFILL_PRIORITY) && nadm > 0);
+    if (credit || decode_all) {
+      for (int c0 = 0; c0 < R0; c0 += 32) {
+        int j = c0 + lane;
+        bool b = false;
+        if (j < R0) {
+          if (credit) {  // select_batch, sched_scorpio.py:171-179
+            RRec& r = s.rr[j];
+            if constexpr (WIDE) {
+              cred_t<WIDE> N = ((unsigned __int128)s.rNhi[j] << 64) | r.N;
+              cred_t<WIDE> S = ((unsigned __int128)s.rShi[j] << 64) | r.S;
+              N += MIN;
+              if (N >= S) {
+                N -= S;
+                b = true;
+              }
+              r.N = (uint64_t)N;
+              s.rNhi[j] = (uint64_t)(N >> 64);
+            } else {
+              uint64_t N = r.N + MIN;
+              if (N >= r.S) {
+                N -= r.S;
+                b = true;
+              }
+              r.N = N;
+            }
+          } else {
+            b = true;
+          }
+        }
+        unsigned bm = __ballot_sync(SL_FULL, b);
+        if (b) {
+          RRec& r = s.rr[j];
+          int pos = nbatch + __popc(bm & lanemask_lt());
+          blen += r.cur_len;
+          r.cur_len += 1;  // token emit (simengine.py:243-245); l_avg already taken
+          r.rem -= 1;
+          int64_t rid = s.id[s.rl[j]];
+          acc.dig += digest_item((uint64_t)step, 2, (uint32_t)pos, (uint64_t)rid);
+          if (lg_bat >= 0 && pos < cap_bat) a.log.batch_ids[lg_bat + pos] = rid;
+        }
+        nbatch += __popc(bm);
+      }
+    }
+
+    // ---- no work: idle skip (simengine.py:207-227)
+    if (nadm == 0 && nbatch == 0) {
+      double dl = kInf;
+      for (int j = lane; j < W; j += 32) {
+        double d = s.wr[s.wl[j]].deadline;
+        if (d > now && d < dl) dl = d;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) dl = fmin(dl, __shfl_xor_sync(SL_FULL, dl, o));
+      bool have = dl != kInf;
+      double target = dl;
+      if (next < n) {
+        if (!have || next_t < target) target = next_t;
+        have = true;
+      } else if (R > 0) {
+        status = SL_SIM_NO_WORK_RUNNING;
+        break;
+      }
+      if (!have) {
+        if (W > 0) status = SL_SIM_NO_PROGRESS;
+        break;
+      }
+      if (target <= now) {
+        status = SL_SIM_NO_PROGRESS;
+        break;
+      }
+      n_idle++;
+      now = target;
+      continue;
+    }
+
+    // ---- step duration (simengine.py:233-238)
+    double prefill_s = ps_result(P);
+    double decode_s = 0.0;
+    int64_t bl = warp_sum_i64(blen);
+    if (nbatch > 0) decode_s = itl(C, nbatch, fdiv_((double)bl, (double)nbatch));
+    double end = fadd_(fadd_(now, prefill_s), decode_s);
+    acc.dig += acc.dig_rej;
+    if (lane == 0) acc.dig += digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
+
+    // ---- decision log row
+    if (logging) {
+      bool fits = !log_over && step < a.log.step_cap && cur_adm + nadm <= a.log.id_cap &&
+                  cur_rej + nrej <= a.log.id_cap && cur_batch + nbatch <= a.log.id_cap;
+      if (fits) {
+        double vbs = 0.0, mslo = __longlong_as_double(0x7ff8000000000000LL);
+        if (scorpio && R > 0) {  // sched_scorpio.py:312-315 (before retirement); baselines keep defaults
+          mslo = fixed_to_double<WIDE>(MIN, s.pow2E);
+          PySum vs;
+          ps_init(vs);
+          for (int c0 = 0; c0 < R; c0 += 32) {
+            int j = c0 + lane;
+            double x = 0.0;
+            if (j < R) x = fdiv_(mslo, fixed_to_double<WIDE>(load_S<WIDE>(s, j), s.pow2E));
+            int cnt = min(32, R - c0);
+            for (int t = 0; t < cnt; ++t) ps_add(vs, bcast(x, t));
+          }
+          vbs = ps_result(vs);
+        }
+        if (lane == 0) {
+          int64_t o = lg_step0 + step;
+          a.log.now[o] = now;
+          a.log.end[o] = end;
+          a.log.prefill_s[o] = prefill_s;
+          a.log.decode_s[o] = decode_s;
+          a.log.vbs[o] = vbs;
+          a.log.min_slo[o] = mslo;
+          a.log.n_admitted[o] = nadm;
+          a.log.n_rejected[o] = nrej;
+          a.log.n_batch[o] = nbatch;
+          a.log.n_steps[s.log_row] = step + 1;
+        }
+        cur_adm += nadm;
+        cur_rej += nrej;
+        cur_batch += nbatch;
+      } else {
+        log_over = true;
+      }
+    }
+
+    // ---- emits for fresh entries + retirement (simengine.py:240-271)
+    int keptR = 0;
+    for (int c0 = 0; c0 < R; c0 += 32) {
+      int j = c0 + lane;
+      bool valid = j < R;
+      RRec r;
+      int idx = 0;
+      uint64_t nhi = 0, shi = 0;
+      bool ret = false;
+      if (valid) {
+        r = s.rr[j];
+        idx = s.rl[j];
+        if constexpr (WIDE) {
+          nhi = s.rNhi[j];
+          shi = s.rShi[j];
+        }
+        if (j >= R0) {  // admitted this step: tokens = 1, first emit at `end`
+          r.cur_len += 1;
+          r.rem -= 1;
+          s.first_emit[idx] = end;
+        }
+        ret = r.rem <= 0;
+      }
+      unsigned km = __ballot_sync(SL_FULL, valid && !ret);
+      __syncwarp();
+      if (valid && !ret) {
+        int q = keptR + __popc(km & lanemask_lt());
+        s.rr[q] = r;
+        s.rl[q] = idx;
+        if constexpr (WIDE) {
+          s.rNhi[q] = nhi;
+          s.rShi[q] = shi;
+        }
+      }
+      if (ret) {
+        const WRec& w = s.wr[idx];
+        double first = j >= R0 ? end : s.first_emit[idx];
+        int32_t tout = s.true_out[idx];
+        double tpot = tout == 1 ? 0.0 : fdiv_(fsub_(end, first), (double)(tout - 1));
+        double ttft = fsub_(first, w.arr);
+        bool ok = ttft <= w.ttft && tpot <= w.tpot;
+        acc.completed++;
+        acc.compliant += ok;
+        acc.ttft_viol += ttft > w.ttft;
+        acc.tpot_viol += tpot > w.tpot;
+        if (has_out) {
+          int64_t o = s.out_off + idx;
+          a.out.status[o] = SL_COMPLETED;
+          a.out.compliant[o] = ok;
+          a.out.completion_step[o] = (int32_t)step;
+          a.out.first_token_time[o] = first;
+          a.out.completion_time[o] = end;
+          a.out.ttft[o] = ttft;
+          a.out.tpot[o] = tpot;
+        }
+      }
+      __syncwarp();
+      keptR += __popc(km);
+    }
+    R = keptR;
+    now = end;
+    step++;
+  }
+
+  // ---- result row (summarize/goodput/adherence, report.py:71-134)
+  uint64_t dig = warp_sum_u64(acc.dig);
+  int64_t completed = warp_sum_i64(acc.completed);
+  int64_t compliant = warp_sum_i64(acc.compliant);
+  int64_t rj_t = warp_sum_i64(acc.rej_ttft);
+  int64_t rj_a = warp_sum_i64(acc.rej_adm);
+  int64_t tv = warp_sum_i64(acc.ttft_viol);
+  int64_t pv = warp_sum_i64(acc.tpot_viol);
+  if (lane == 0) {
+    sl_result res;
+    res.status = status | (log_over ? SL_SIM_LOG_OVERFLOW : 0);
+    res._pad = 0;
+    res.n_steps = step;
+    res.n_plans = n_plans;
+    res.n_idle_skips = n_idle;
+    res.request_steps = req_steps;
+    res.total = n;
+    res.completed = completed;
+    res.compliant = compliant;
+    res.rejected_ttft = rj_t;
+    res.rejected_admission = rj_a;
+    res.incomplete = n - completed - rj_t - rj_a;
+    res.ttft_violations = tv;
+    res.tpot_violations = pv;
+    res.sim_end = now;
+    double h = has_h ? s.horizon : (now > 1e-12 ? now : 1e-12);
+    res.horizon = h;
+    res.goodput = fdiv_((double)compliant, h);
+    res.adherence = n > 0 ? fdiv_((double)compliant, (double)n) : 0.0;
+    res.digest = dig;
+    a.results[sim_index] = res;
+  }
+}
+
+__global__ void __launch_bounds__(128) sl_sim_kernel(const __grid_constant__ KArgs a) {
+  const int lane = threadIdx.x & 31;
+  Workspace ws = carve(a.ws_base, a.slots);
+  for (;;) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(ws.counter, 1);
+    q = __shfl_sync(SL_FULL, q, 0);
+    if (q >= a.n_sims) return;
+    int si = a.order ? a.order[q] : q;
+    const sl_sim& sp = a.sims[si];
+    Sim s;
+    int t = sp.trace;
+    int64_t b = a.tr.begin[t];
+    s.n = a.tr.begin[t + 1] - b;
+    s.arrival = a.tr.arrival + b;
+    s.ttft_b = a.tr.ttft_slo + b;
+    s.tpot_b = a.tr.tpot_slo + b;
+    s.prompt = a.tr.prompt_len + b;
+    s.true_out = a.tr.true_out + b;
+    s.predicted = a.tr.predicted + b;
+    s.id = a.tr.id + b;
+    s.cost = sp.cost;
+    s.scale = sp.slo_scale;
+    s.factor = sp.rate_factor;
+    s.horizon = sp.horizon;
+    s.policy = sp.policy;
+    s.flags = sp.flags;
+    s.cap = sp.max_batch_size;
+    s.E = sp.credit_exp;
+    s.pow2E = __longlong_as_double((long long)(sp.credit_exp + 1023) << 52);
+    int64_t o = sp.ws_offset;
+    s.wl = ws.wl + o;
+    s.rl = ws.rl + o;
+    s.wr = ws.wr + o;
+    s.rr = ws.rr + o;
+    s.wShi = ws.wShi + o;
+    s.rNhi = ws.rNhi + o;
+    s.rShi = ws.rShi + o;
+    s.first_emit = ws.first_emit + o;
+    s.out_off = sp.out_offset;
+    s.log_row = sp.log_slot;
+    bool has_out = a.has_out && sp.out_offset >= 0;
+    if (sp.credit_wide)
+      run_sim<true>(s, a, has_out, si, lane);
+    else
+      run_sim<false>(s, a, has_out, si, lane);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t sl_workspace_bytes(int64_t total_slots, int32_t n_sims) {
+  (void)n_sims;
+  return workspace_bytes(total_slots);
+}
+
+int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_t* credit_exp,
+                     int32_t* credit_wide) {
+  if (!credit_exp || !credit_wide || (n > 0 && !tpot_slo)) return SL_ERR_ARG;
+  int e_min = 1 << 30, e_max = -(1 << 30);
+  for (int64_t i = 0; i < n; i++) {
+    double v = tpot_slo[i] * slo_scale;
+    if (!(v > 0.0) || !isfinite(v) || !isnormal(v)) return SL_ERR_ARG;
+    int e;
+    frexp(v, &e);
+    if (e < e_min) e_min = e;
+    if (e > e_max) e_max = e;
+  }
+  if (n == 0) {
+    *credit_exp = 0;
+    *credit_wide = 0;
+    return SL_OK;
+  }
+  int E = e_min - 53;
+  if (E < -1022) return SL_ERR_ARG;
+  int span = e_max - e_min;  // S < 2^(53+span); need 2*S <= 2^64 (narrow) / 2^128 (wide)
+  *credit_exp = E;
+  *credit_wide = (53 + span + 1 > 64) ? 1 : 0;
+  if (53 + span + 1 > 128) return SL_ERR_ARG;
+  return SL_OK;
+}
+
+int sl_run_batch_launches(void) { return 1; }
+
+int sl_abi_layout(int64_t* out, int32_t n) {
+  if (!out || n < 6) return SL_ERR_ARG;
+  out[0] = sizeof(sl_sim);
+  out[1] = sizeof(sl_result);
+  out[2] = sizeof(sl_traces);
+  out[3] = sizeof(sl_outcomes);
+  out[4] = sizeof(sl_log);
+  out[5] = sizeof(sl_cost);
+  return SL_OK;
+}
+
+int sl_device_info(int32_t* sm_count, int32_t* l2_bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SL_ERR_NO_DEVICE;
+  int v = 0;
+  if (sm_count) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    *sm_count = v;
+  }
+  if (l2_bytes) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+    *l2_bytes = v;
+  }
+  return SL_OK;
+}
+
+int sl_run_batch(const sl_traces* traces, const sl_sim* sims, const int32_t* order, int32_t n_sims,
+                 void* workspace, int64_t total_slots, sl_result* results,
+                 const sl_outcomes* outcomes, const sl_log* log, void* stream) {
+  if (!traces || !sims || !workspace || !results || n_sims < 0 || total_slots < 0)
+    return SL_ERR_ARG;
+  if (n_sims == 0) return SL_OK;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.tr = *traces;
+  a.sims = sims;
+  a.order = order;
+  a.n_sims = n_sims;
+  a.slots = total_slots;
+  a.ws_base = workspace;
+  a.results = results;
+  if (outcomes) {
+    a.out = *outcomes;
+    a.has_out = 1;
+  }
+  if (log) {
+    a.log = *log;
+    a.has_log = 1;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(workspace, 0, 256, st) != cudaSuccess) return SL_ERR_CUDA;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sl_sim_kernel, 128, 0);
+  if (per_sm < 1) per_sm = 1;
+  int64_t warps_needed = n_sims;
+  int64_t blocks = (warps_needed + 3) / 4;
+  int64_t max_blocks = (int64_t)sms * per_sm;
+  if (blocks > max_blocks) blocks = max_blocks;
+  sl_sim_kernel<<<(unsigned)blocks, 128, 0, st>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return SL_ERR_CUDA;
+  return SL_OK;
+}
+
+}  // extern "C"
