@@ -40,7 +40,8 @@ def gpu_run():
     traces, cells = _cells(cases)
     max_steps = max(c["n_steps"] for c in cases) + 1
     max_ids = max(len(c["log"]["ids"]) if c["keep_log"] else 0 for c in cases) + 1
-    eng = BatchEngine(traces, cells, outcomes=True, log_cells=list(range(len(cells))),
+    log_cells = [k for k, c in enumerate(cases) if c["keep_log"]]
+    eng = BatchEngine(traces, cells, outcomes=True, log_cells=log_cells,
                       log_steps=max_steps, log_ids=max_ids)
     eng.launch()
     res = eng.results()
