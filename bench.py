@@ -1,0 +1,336 @@
+"""Benchmark: Scorpio scheduler request-steps/s on B200 (config 3 / config 5 sweep).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU, NCCL)
+
+One "step" = one pass of the hot path over one batch: every simulation cell of
+the rank's shard of the config-3 grid (64 request rates x 64 SLO scales of 10k
+requests each = 4,096 sims per GPU; N GPUs sweep 4,096*N cells = config 5 at
+N=8, weak scaling) run to completion by one sl_run_batch launch, followed by
+the NCCL all_gather of the per-sim result rows when N > 1.
+
+metric: request-steps/s, where one request-step = one waiting or running
+request at plan_step entry processed by one scheduler iteration of one sim
+(SURVEY 8(d)); the device counts them exactly per sim.
+
+`--impl reference` times the reference algorithm's CPU implementation (the C
+restatement under oracle/, the reference itself being pure Python that cannot
+travel to the GPU box) on all host threads over a bounded sample of the same
+cells and prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_REQUEST_STEP = 56  # algorithmic bytes per request-step
+METRIC = "scheduler request-steps/sec"
+UNIT = "request-steps/s"
+
+
+def peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi style clock/throttle sampling during the timed region (NVML)."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self) -> dict:
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def make_grid(args, world: int):
+    from paper_2505_23022_b200.sweep import SweepGrid
+
+    rates = tuple(np.linspace(2.0, 32.0, args.rates))
+    scales = tuple(np.geomspace(0.5, 2.0, args.scales * world))
+    return SweepGrid(rates=rates, scales=scales, n_requests=args.n_requests)
+
+
+def sample_cells(grid, n_sample: int) -> list[tuple[int, int]]:
+    """Stratified (rate, scale) sample across the grid for the CPU baseline."""
+    nr, ns = len(grid.rates), len(grid.scales)
+    side = max(1, int(round(np.sqrt(n_sample))))
+    ri = np.unique(np.linspace(0, nr - 1, side).round().astype(int))
+    si = np.unique(np.linspace(0, ns - 1, max(1, n_sample // len(ri))).round().astype(int))
+    return [(int(a), int(b)) for a in ri for b in si]
+
+
+def cpu_reference(grid, n_sample: int, budget_s: float, threads: int):
+    """Time the C restatement (oracle/) on all host threads over a bounded sample.
+
+    Returns (request_steps, seconds, n_cells, cells_desc)."""
+    from oracle import oracle as orc
+
+    pairs = sample_cells(grid, n_sample)
+    traces = {}
+    jobs = []
+    cfg = grid.config
+    for ri, si in pairs:
+        if ri not in traces:
+            traces[ri] = grid.trace_for_rate(grid.rates[ri])
+        t = traces[ri]
+        s = float(grid.scales[si])
+        jobs.append(dict(arrival=t.arrival, ttft_slo=t.ttft_slo * s, tpot_slo=t.tpot_slo * s,
+                         prompt_len=t.prompt_len, true_out=t.true_out, ids=t.id,
+                         predicted=t.predicted,
+                         params=orc.make_params(itl=cfg.itl, prefill=cfg.prefill)))
+    orc.lib()
+    rs, done = 0, 0
+    t0 = time.perf_counter()
+    # run in waves of `threads` cells until the time budget is used
+    for k in range(0, len(jobs), threads):
+        out = orc.run_many(jobs[k:k + threads], threads=threads)
+        rs += sum(o["summary"]["request_steps"] for o in out)
+        done += len(out)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return rs, dt, done, f"{done} of {grid.n_cells} cells (stratified rate x scale), " \
+                         f"{grid.n_requests} requests each"
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    grid = make_grid(args, 1)
+    steps_rs, steps_dt = [], []
+    desc = ""
+    for it in range(args.warmup + args.steps):
+        rs, dt, n, desc = cpu_reference(grid, args.cpu_sample, args.cpu_budget, threads)
+        if it >= args.warmup:
+            steps_rs.append(rs)
+            steps_dt.append(dt)
+    value = sum(steps_rs) / sum(steps_dt)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(steps_dt) / len(steps_dt), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
+            "config": {"workload": "config3 sweep sample", "n_requests": grid.n_requests},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_23022_b200 import _native as N
+    from paper_2505_23022_b200.sweep import build_local, gather_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    grid = make_grid(args, world)
+    t_setup = time.perf_counter()
+    eng, owned, traces = build_local(grid, rank, world, device=dev)
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream(dev)
+    l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def one_step():
+        eng.launch(stream)
+        if world > 1:
+            gather_rows(eng.results_device(), owned, grid.n_cells)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    res = eng.results()
+    assert ((res["status"] & 3) == 0).all(), "engine error in a sim"
+    local_rs = int(res["request_steps"].sum())
+
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            l2.zero_()  # flush L2 between timed iterations
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    # kernel-only time (for the roofline): the launch alone, same stream
+    ktimes = []
+    for _ in range(max(1, min(args.steps, 3))):
+        l2.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.launch(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ktimes.append(e0.elapsed_time(e1) / 1e3)
+
+    # e2e: public API with host buffers; H2D of inputs + launch + D2H of result rows
+    pinned = {k: v.cpu().pin_memory() for k, v in eng._tr.items()}
+    sims_pinned = eng._sims.cpu().pin_memory()
+    res_pinned = torch.empty(eng._res.numel(), dtype=torch.uint8).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in pinned.values()) + sims_pinned.numel()
+    d2h = res_pinned.numel()
+    etimes = []
+    for _ in range(args.steps):
+        l2.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k, v in pinned.items():
+            eng._tr[k].copy_(v, non_blocking=True)
+        eng._sims.copy_(sims_pinned, non_blocking=True)
+        one_step()
+        res_pinned.copy_(eng._res, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        etimes.append(e0.elapsed_time(e1) / 1e3)
+
+    t_step = float(np.mean(times))
+    t_kernel = float(np.mean(ktimes))
+    t_e2e = float(np.mean(etimes))
+    if world > 1:
+        v = torch.tensor([t_step, t_kernel, t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        t_step, t_kernel, t_e2e = (float(x) for x in v.tolist())
+        n = torch.tensor([local_rs], dtype=torch.int64, device=dev)
+        dist.all_reduce(n)
+        total_rs = int(n.item())
+    else:
+        total_rs = local_rs
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        rs, dt, ncell, desc = cpu_reference(grid, args.cpu_sample, args.cpu_budget, threads)
+        cpu = {"value": rs / dt, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        peak, src = peaks()
+        achieved = local_rs * BYTES_PER_REQUEST_STEP / t_kernel / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "sim_kernel_traffic.json")
+        if os.path.exists(prof):
+            p = json.load(open(prof))
+            if p.get("n_requests") == args.n_requests and p.get("cells") == eng.n_sims:
+                traffic = p.get("dram_bytes")
+        line = {
+            "metric": METRIC, "value": total_rs / t_step, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64+int64", "data": "synthetic (reference workload generator, seeded)",
+            "config": {"workload": f"config{'5' if world > 1 else '3'}: "
+                                   f"{len(grid.rates)} rates x {len(grid.scales)} SLO scales "
+                                   f"sweep, {grid.n_requests} requests/sim",
+                       "sims": grid.n_cells, "sims_per_gpu": eng.n_sims,
+                       "n_requests": grid.n_requests, "request_steps": total_rs,
+                       "parallelism": f"sim-sharded x{world}", "l2": "flushed between steps",
+                       "setup_s": round(setup_s, 2)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": src,
+                         "bytes_per_unit": BYTES_PER_REQUEST_STEP,
+                         "kernel": "sl_sim_kernel", "kernel_ms": 1e3 * t_kernel},
+            "cpu_baseline": cpu,
+            "e2e": {"value": total_rs / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps * N.lib().sl_run_batch_launches(),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rates", type=int, default=64)
+    ap.add_argument("--scales", type=int, default=64, help="SLO scales per GPU")
+    ap.add_argument("--n-requests", type=int, default=10_000)
+    ap.add_argument("--cpu-sample", type=int, default=64)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
