@@ -41,6 +41,7 @@ extern "C" {
 #define SL_SIM_NO_WORK_RUNNING 1 /* EngineError simengine.py:217 */
 #define SL_SIM_NO_PROGRESS 2     /* EngineError simengine.py:220,224 */
 #define SL_SIM_LOG_OVERFLOW 4    /* decision log capacity exceeded (run continues) */
+#define SL_SIM_CAPACITY 8        /* fast kernel handoff: rerun by the general kernel (never final) */
 
 /* ---- request status (core.Status, core.py:19-25) ----------------------- */
 #define SL_COMPLETED 0
@@ -60,6 +61,11 @@ extern "C" {
 #define SL_FLAG_R_ONLY 4
 #define SL_FLAG_HAS_HORIZON 8
 #define SL_FLAG_PREFILL_PRIORITY 16
+#define SL_FLAG_GENERAL_ONLY 32 /* host: skip the register-resident fast kernel */
+
+/* ---- sl_run_batch_ex modes --------------------------------------------- */
+#define SL_MODE_AUTO 0    /* fast kernel, then the general kernel for handoffs */
+#define SL_MODE_GENERAL 1 /* general kernel only (parity cross-check) */
 
 typedef struct {
   double alpha, beta, gamma, delta, epsilon; /* ItlParams, costmodel.py:31-47 */
@@ -165,6 +171,11 @@ int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_
 int sl_run_batch(const sl_traces* traces, const sl_sim* sims, const int32_t* order, int32_t n_sims,
                  void* workspace, int64_t total_slots, sl_result* results,
                  const sl_outcomes* outcomes, const sl_log* log, void* stream);
+
+/* sl_run_batch with an explicit SL_MODE_*. */
+int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* order,
+                    int32_t n_sims, void* workspace, int64_t total_slots, sl_result* results,
+                    const sl_outcomes* outcomes, const sl_log* log, int32_t mode, void* stream);
 
 /* Number of kernels sl_run_batch launches per call (for the gpu_launches claim). */
 int sl_run_batch_launches(void);

@@ -34,6 +34,9 @@ COMPLETED, REJECTED_TTFT, REJECTED_ADMISSION, INCOMPLETE = 0, 1, 2, 3
 POLICY = {"scorpio": 0, "greedy": 1, "sjf": 2, "early_reject": 3}
 FLAG_TTFT_GUARD, FLAG_TPOT_GUARD, FLAG_R_ONLY, FLAG_HAS_HORIZON, FLAG_PREFILL_PRIORITY = (
     1, 2, 4, 8, 16)
+FLAG_GENERAL_ONLY = 32
+SIM_CAPACITY = 8
+MODE_AUTO, MODE_GENERAL = 0, 1
 
 COST_FIELDS = ("alpha", "beta", "gamma", "delta", "epsilon", "phi", "theta", "alpha_p", "beta_p")
 
@@ -112,6 +115,10 @@ def lib():
                                C.c_int64, C.c_void_p, C.POINTER(SlOutcomes), C.POINTER(SlLog),
                                C.c_void_p]
     L.sl_run_batch.restype = C.c_int
+    L.sl_run_batch_ex.argtypes = [C.POINTER(SlTraces), C.c_void_p, C.c_void_p, C.c_int32,
+                                  C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(SlOutcomes),
+                                  C.POINTER(SlLog), C.c_int32, C.c_void_p]
+    L.sl_run_batch_ex.restype = C.c_int
     L.sl_run_batch_launches.restype = C.c_int
     L.sl_abi_layout.argtypes = [C.POINTER(C.c_int64), C.c_int32]
     L.sl_abi_layout.restype = C.c_int

@@ -123,6 +123,9 @@ def pack_cells(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = Fa
     """Build the sl_sim table (host); workspace/outcome offsets by prefix sum."""
     sims = np.zeros(len(cells), N.SIM_DTYPE)
     uniq = [np.unique(t.tpot_slo) for t in traces]
+    # the fast kernel sums up to 64 current lengths in 32 bits
+    huge = [bool(len(t) and int((t.prompt_len.astype(np.int64) + t.true_out).max()) >= 1 << 26)
+            for t in traces]
     ws = 0
     log_rows = {c: r for r, c in enumerate(log_cells or [])}
     for k, c in enumerate(cells):
@@ -144,7 +147,7 @@ def pack_cells(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = Fa
         s = sims[k]
         s["trace"] = c.trace
         s["policy"] = N.POLICY[cfg.policy]
-        s["flags"] = cfg.flags()
+        s["flags"] = cfg.flags() | (N.FLAG_GENERAL_ONLY if huge[c.trace] else 0)
         s["max_batch_size"] = cfg.max_batch_size
         s["slo_scale"] = c.slo_scale
         s["rate_factor"] = c.rate_factor
@@ -166,7 +169,7 @@ class BatchEngine:
     def __init__(self, traces: list[TraceArrays], cells: list[Cell] | np.ndarray,
                  outcomes: bool = False, log_cells: list[int] | None = None,
                  log_steps: int = 0, log_ids: int = 0, order: np.ndarray | None = None,
-                 device=None):
+                 device=None, mode: int = N.MODE_AUTO):
         torch = N.require_cuda()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
@@ -176,6 +179,7 @@ class BatchEngine:
             sims = pack_cells(traces, cells, outcomes, log_cells)
         self.n_sims = len(sims)
         self.sims_host = sims
+        self.mode = mode
         lens = np.array([len(t) for t in traces], np.int64)
         begin = np.zeros(len(traces) + 1, np.int64)
         np.cumsum(lens, out=begin[1:])
@@ -239,11 +243,11 @@ class BatchEngine:
         """One sl_run_batch on `stream` (default: torch's current stream)."""
         torch = self.torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        rc = N.lib().sl_run_batch(
+        rc = N.lib().sl_run_batch_ex(
             C.byref(self.st), self._sims.data_ptr(), self._order.data_ptr(), self.n_sims,
             self._ws.data_ptr(), self.total_slots, self._res.data_ptr(),
             C.byref(self.oc) if self.oc is not None else None,
-            C.byref(self.lg) if self.lg is not None else None, s.cuda_stream)
+            C.byref(self.lg) if self.lg is not None else None, self.mode, s.cuda_stream)
         if rc != 0:
             raise RuntimeError(f"sl_run_batch failed with code {rc}")
 
@@ -300,9 +304,10 @@ def default_order(traces: list[TraceArrays], sims: np.ndarray) -> np.ndarray:
 
 
 def run_batch(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = False,
-              log_cells: list[int] | None = None, log_steps: int = 0, log_ids: int = 0):
+              log_cells: list[int] | None = None, log_steps: int = 0, log_ids: int = 0,
+              mode: int = N.MODE_AUTO):
     """Convenience: build, launch, and return (results, engine)."""
     eng = BatchEngine(traces, cells, outcomes=outcomes, log_cells=log_cells,
-                      log_steps=log_steps, log_ids=log_ids)
+                      log_steps=log_steps, log_ids=log_ids, mode=mode)
     eng.launch()
     return eng.results(), eng

@@ -23,177 +23,12 @@
 
 #include "scorpio_b200.h"
 #include "sl_device.cuh"
+#include "sim_common.cuh"
+#include "sim_fast.cuh"
 
 using namespace sl;
 
 namespace {
-
-struct __align__(16) WRec {  // per request, written at arrival (WaitingItem + Request fields)
-  double arr;       // arrival_time / rate_factor
-  double ttft;      // ttft_slo * slo_scale
-  double prefill;   // prefill_time(prompt_len), costmodel.py:132-138
-  double tpot;      // tpot_slo * slo_scale
-  double inv;       // 1.0 / tpot
-  double deadline;  // arr + ttft, core.py:50-53
-  uint64_t S;       // fixed-point tpot (low 64 bits)
-  int32_t prompt;
-  int32_t pred_solo;  // predicted_len | solo_ok << 31
-};
-static_assert(sizeof(WRec) == 64, "WRec layout");
-
-struct __align__(16) RRec {  // per running entry, positional (RunningEntry)
-  uint64_t N;   // credit * slo / 2^E (low 64 bits)
-  uint64_t S;   // slo / 2^E (low 64 bits)
-  double inv;   // 1.0 / tpot
-  int32_t cur_len;  // prompt_len + tokens_generated
-  int32_t rem;      // true_output_len - tokens_generated
-};
-static_assert(sizeof(RRec) == 32, "RRec layout");
-
-struct Workspace {  // SoA regions over all request slots
-  int* counter;
-  int32_t* wl;       // waiting list (request index), per sim [n]
-  int32_t* rl;       // running list (request index), per sim [n]
-  WRec* wr;          // per request
-  RRec* rr;          // per running position
-  uint64_t* wShi;    // wide credits: S high word per request
-  uint64_t* rNhi;    // wide credits: per running position
-  uint64_t* rShi;
-  double* first_emit;  // per request
-};
-
-__host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
-
-__host__ __device__ inline Workspace carve(void* base, int64_t slots) {
-  Workspace w;
-  char* p = (char*)base;
-  int64_t off = 0;
-  w.counter = (int*)(p + off);
-  off += 256;
-  w.wl = (int32_t*)(p + off);
-  off = align256(off + slots * 4);
-  w.rl = (int32_t*)(p + off);
-  off = align256(off + slots * 4);
-  w.wr = (WRec*)(p + off);
-  off = align256(off + slots * 64);
-  w.rr = (RRec*)(p + off);
-  off = align256(off + slots * 32);
-  w.wShi = (uint64_t*)(p + off);
-  off = align256(off + slots * 8);
-  w.rNhi = (uint64_t*)(p + off);
-  off = align256(off + slots * 8);
-  w.rShi = (uint64_t*)(p + off);
-  off = align256(off + slots * 8);
-  w.first_emit = (double*)(p + off);
-  return w;
-}
-
-__host__ __device__ inline int64_t workspace_bytes(int64_t slots) {
-  return 256 + 8 * 256 + align256(slots * 4) * 2 + align256(slots * 64) + align256(slots * 32) +
-         align256(slots * 8) * 4;
-}
-
-struct KArgs {
-  sl_traces tr;
-  const sl_sim* sims;
-  const int32_t* order;
-  int32_t n_sims;
-  int64_t slots;
-  void* ws_base;
-  sl_result* results;
-  sl_outcomes out;
-  int has_out;
-  sl_log log;
-  int has_log;
-};
-
-// Per-sim view, warp-uniform.
-struct Sim {
-  // trace
-  const double* arrival;
-  const double* ttft_b;
-  const double* tpot_b;
-  const int32_t* prompt;
-  const int32_t* true_out;
-  const int32_t* predicted;
-  const int64_t* id;
-  int64_t n;
-  // params
-  sl_cost cost;
-  double scale, factor, horizon, pow2E;
-  int policy, flags, cap, E;
-  // workspace slices
-  int32_t* wl;
-  int32_t* rl;
-  WRec* wr;
-  RRec* rr;
-  uint64_t* wShi;
-  uint64_t* rNhi;
-  uint64_t* rShi;
-  double* first_emit;
-  // outputs
-  int64_t out_off;
-  int64_t log_row;
-};
-
-__device__ __forceinline__ bool key_less_ldf(const Sim& s, double da, double aa, int ia, double db,
-                                             double ab, int ib) {
-  // sort_key = (deadline, arrival_time, id), schedtypes.py:28-32
-  if (da != db) return da < db;
-  if (aa != ab) return aa < ab;
-  return s.id[ia] < s.id[ib];
-}
-
-__device__ __forceinline__ bool key_less_sjf(const Sim& s, int32_t pa, double aa, int ia,
-                                             int32_t pb, double ab, int ib) {
-  // sched_baselines.py:138-142 key (predicted_len, arrival_time, id)
-  if (pa != pb) return pa < pb;
-  if (aa != ab) return aa < ab;
-  return s.id[ia] < s.id[ib];
-}
-
-// Insert request `idx` into the sorted waiting list at its rank (keys are
-// unique, so rank == bisect position).  Warp-cooperative: O(W/32) compares
-// and a top-down chunked shift.
-__device__ void insert_sorted(const Sim& s, int& W, int idx, bool sjf, int lane) {
-  const WRec& me = s.wr[idx];
-  double dk = me.deadline, ak = me.arr;
-  int32_t pk = me.pred_solo & 0x7fffffff;
-  int pos = 0;
-  for (int c0 = 0; c0 < W; c0 += 32) {
-    int j = c0 + lane;
-    bool lt = false;
-    if (j < W) {
-      int o = s.wl[j];
-      const WRec& r = s.wr[o];
-      lt = sjf ? key_less_sjf(s, r.pred_solo & 0x7fffffff, r.arr, o, pk, ak, idx)
-               : key_less_ldf(s, r.deadline, r.arr, o, dk, ak, idx);
-    }
-    pos += __popc(__ballot_sync(SL_FULL, lt));
-  }
-  // shift [pos, W) up by one, highest chunk first
-  int tail = W - pos;
-  for (int c = (tail - 1) / 32; c >= 0 && tail > 0; --c) {
-    int j = pos + c * 32 + lane;
-    int v = 0;
-    bool ok = j < W;
-    if (ok) v = s.wl[j];
-    __syncwarp();
-    if (ok) s.wl[j + 1] = v;
-    __syncwarp();
-  }
-  if (lane == 0) s.wl[pos] = idx;
-  __syncwarp();
-  W += 1;
-}
-
-// Per-lane accumulators folded into the result row at the end.
-struct Acc {
-  uint64_t dig;       // committed digest partial
-  uint64_t dig_rej;   // pending (rejections of the current plan)
-  int64_t completed, compliant, rej_ttft, rej_adm, ttft_viol, tpot_viol;
-  int64_t prej_ttft, prej_adm;  // (counted immediately; outcomes are final)
-};
 
 // TTFT prefix walk over wl[0, W) in list order (ttft_guard :196-205 /
 // early_reject sched_baselines.py:95-103).  Rejected -> REJECTED_TTFT.
@@ -725,42 +560,40 @@ __device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_inde
     step++;
   }
 
-  // ---- result row (summarize/goodput/adherence, report.py:71-134)
-  uint64_t dig = warp_sum_u64(acc.dig);
-  int64_t completed = warp_sum_i64(acc.completed);
-  int64_t compliant = warp_sum_i64(acc.compliant);
-  int64_t rj_t = warp_sum_i64(acc.rej_ttft);
-  int64_t rj_a = warp_sum_i64(acc.rej_adm);
-  int64_t tv = warp_sum_i64(acc.ttft_viol);
-  int64_t pv = warp_sum_i64(acc.tpot_viol);
-  if (lane == 0) {
-    sl_result res;
-    res.status = status | (log_over ? SL_SIM_LOG_OVERFLOW : 0);
-    res._pad = 0;
-    res.n_steps = step;
-    res.n_plans = n_plans;
-    res.n_idle_skips = n_idle;
-    res.request_steps = req_steps;
-    res.total = n;
-    res.completed = completed;
-    res.compliant = compliant;
-    res.rejected_ttft = rj_t;
-    res.rejected_admission = rj_a;
-    res.incomplete = n - completed - rj_t - rj_a;
-    res.ttft_violations = tv;
-    res.tpot_violations = pv;
-    res.sim_end = now;
-    double h = has_h ? s.horizon : (now > 1e-12 ? now : 1e-12);
-    res.horizon = h;
-    res.goodput = fdiv_((double)compliant, h);
-    res.adherence = n > 0 ? fdiv_((double)compliant, (double)n) : 0.0;
-    res.digest = dig;
-    a.results[sim_index] = res;
+  write_result(a, sim_index, acc, status | (log_over ? SL_SIM_LOG_OVERFLOW : 0), n, step,
+               n_plans, n_idle, req_steps, now, has_h, s.horizon, lane);
+}
+
+// General kernel: waiting and running lists in global memory (any size).
+// handoff_only: run just the sims the fast kernel handed off (SL_SIM_CAPACITY).
+__global__ void __launch_bounds__(128) sl_sim_kernel(const __grid_constant__ KArgs a,
+                                                     int handoff_only) {
+  const int lane = threadIdx.x & 31;
+  Workspace ws = carve(a.ws_base, a.slots);
+  for (;;) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(ws.counter + 1, 1);
+    q = __shfl_sync(SL_FULL, q, 0);
+    if (q >= a.n_sims) return;
+    int si = a.order ? a.order[q] : q;
+    if (handoff_only && !(a.results[si].status & SL_SIM_CAPACITY)) continue;
+    Sim s = make_sim(a, ws, si);
+    bool has_out = a.has_out && s.out_off >= 0;
+    if (a.sims[si].credit_wide)
+      run_sim<true>(s, a, has_out, si, lane);
+    else
+      run_sim<false>(s, a, has_out, si, lane);
   }
 }
 
-__global__ void __launch_bounds__(128) sl_sim_kernel(const __grid_constant__ KArgs a) {
+// Fast kernel: running set in registers (sim_fast.cuh); hands off sims that
+// outgrow it or are flagged general-only.
+constexpr int kFastWarps = 4;
+__global__ void __launch_bounds__(32 * kFastWarps) sl_sim_fast_kernel(
+    const __grid_constant__ KArgs a) {
+  __shared__ Slot<false> scratch[kFastWarps][kRunCap];
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   Workspace ws = carve(a.ws_base, a.slots);
   for (;;) {
     int q = 0;
@@ -769,42 +602,13 @@ __global__ void __launch_bounds__(128) sl_sim_kernel(const __grid_constant__ KAr
     if (q >= a.n_sims) return;
     int si = a.order ? a.order[q] : q;
     const sl_sim& sp = a.sims[si];
-    Sim s;
-    int t = sp.trace;
-    int64_t b = a.tr.begin[t];
-    s.n = a.tr.begin[t + 1] - b;
-    s.arrival = a.tr.arrival + b;
-    s.ttft_b = a.tr.ttft_slo + b;
-    s.tpot_b = a.tr.tpot_slo + b;
-    s.prompt = a.tr.prompt_len + b;
-    s.true_out = a.tr.true_out + b;
-    s.predicted = a.tr.predicted + b;
-    s.id = a.tr.id + b;
-    s.cost = sp.cost;
-    s.scale = sp.slo_scale;
-    s.factor = sp.rate_factor;
-    s.horizon = sp.horizon;
-    s.policy = sp.policy;
-    s.flags = sp.flags;
-    s.cap = sp.max_batch_size;
-    s.E = sp.credit_exp;
-    s.pow2E = __longlong_as_double((long long)(sp.credit_exp + 1023) << 52);
-    int64_t o = sp.ws_offset;
-    s.wl = ws.wl + o;
-    s.rl = ws.rl + o;
-    s.wr = ws.wr + o;
-    s.rr = ws.rr + o;
-    s.wShi = ws.wShi + o;
-    s.rNhi = ws.rNhi + o;
-    s.rShi = ws.rShi + o;
-    s.first_emit = ws.first_emit + o;
-    s.out_off = sp.out_offset;
-    s.log_row = sp.log_slot;
-    bool has_out = a.has_out && sp.out_offset >= 0;
-    if (sp.credit_wide)
-      run_sim<true>(s, a, has_out, si, lane);
-    else
-      run_sim<false>(s, a, has_out, si, lane);
+    if ((sp.flags & SL_FLAG_GENERAL_ONLY) || sp.credit_wide) {  // 128-bit credits: general
+      if (lane == 0) a.results[si].status = SL_SIM_CAPACITY;
+      continue;
+    }
+    Sim s = make_sim(a, ws, si);
+    bool has_out = a.has_out && s.out_off >= 0;
+    run_fast<false>(s, a, has_out, si, lane, scratch[warp]);
   }
 }
 
@@ -843,7 +647,7 @@ int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_
   return SL_OK;
 }
 
-int sl_run_batch_launches(void) { return 1; }
+int sl_run_batch_launches(void) { return 2; }
 
 int sl_abi_layout(int64_t* out, int32_t n) {
   if (!out || n < 6) return SL_ERR_ARG;
@@ -871,10 +675,11 @@ int sl_device_info(int32_t* sm_count, int32_t* l2_bytes) {
   return SL_OK;
 }
 
-int sl_run_batch(const sl_traces* traces, const sl_sim* sims, const int32_t* order, int32_t n_sims,
-                 void* workspace, int64_t total_slots, sl_result* results,
-                 const sl_outcomes* outcomes, const sl_log* log, void* stream) {
-  if (!traces || !sims || !workspace || !results || n_sims < 0 || total_slots < 0)
+int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* order,
+                    int32_t n_sims, void* workspace, int64_t total_slots, sl_result* results,
+                    const sl_outcomes* outcomes, const sl_log* log, int32_t mode, void* stream) {
+  if (!traces || !sims || !workspace || !results || n_sims < 0 || total_slots < 0 ||
+      (mode != SL_MODE_AUTO && mode != SL_MODE_GENERAL))
     return SL_ERR_ARG;
   if (n_sims == 0) return SL_OK;
   KArgs a;
@@ -896,18 +701,34 @@ int sl_run_batch(const sl_traces* traces, const sl_sim* sims, const int32_t* ord
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(workspace, 0, 256, st) != cudaSuccess) return SL_ERR_CUDA;
-  int dev = 0, sms = 0, per_sm = 0;
+  int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sl_sim_kernel, 128, 0);
-  if (per_sm < 1) per_sm = 1;
-  int64_t warps_needed = n_sims;
-  int64_t blocks = (warps_needed + 3) / 4;
-  int64_t max_blocks = (int64_t)sms * per_sm;
-  if (blocks > max_blocks) blocks = max_blocks;
-  sl_sim_kernel<<<(unsigned)blocks, 128, 0, st>>>(a);
+  auto grid_for = [&](const void* fn, int threads) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t wpb = threads / 32;
+    int64_t blocks = (n_sims + wpb - 1) / wpb;
+    int64_t max_blocks = (int64_t)sms * per_sm;
+    return (unsigned)(blocks < max_blocks ? blocks : max_blocks);
+  };
+  if (mode == SL_MODE_AUTO) {
+    sl_sim_fast_kernel<<<grid_for((const void*)sl_sim_fast_kernel, 32 * kFastWarps),
+                         32 * kFastWarps, 0, st>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return SL_ERR_CUDA;
+  }
+  sl_sim_kernel<<<grid_for((const void*)sl_sim_kernel, 128), 128, 0, st>>>(
+      a, mode == SL_MODE_AUTO ? 1 : 0);
   if (cudaGetLastError() != cudaSuccess) return SL_ERR_CUDA;
   return SL_OK;
+}
+
+int sl_run_batch(const sl_traces* traces, const sl_sim* sims, const int32_t* order, int32_t n_sims,
+                 void* workspace, int64_t total_slots, sl_result* results,
+                 const sl_outcomes* outcomes, const sl_log* log, void* stream) {
+  return sl_run_batch_ex(traces, sims, order, n_sims, workspace, total_slots, results, outcomes,
+                         log, SL_MODE_AUTO, stream);
 }
 
 }  // extern "C"

@@ -32,8 +32,9 @@ def _cells(cases):
     return traces, cells
 
 
-@pytest.fixture(scope="module")
-def gpu_run():
+@pytest.fixture(scope="module", params=["auto", "general"])
+def gpu_run(request):
+    from paper_2505_23022_b200 import _native as N
     from paper_2505_23022_b200.batch import BatchEngine
 
     cases = load_cases()
@@ -41,8 +42,9 @@ def gpu_run():
     max_steps = max(c["n_steps"] for c in cases) + 1
     max_ids = max(len(c["log"]["ids"]) if c["keep_log"] else 0 for c in cases) + 1
     log_cells = [k for k, c in enumerate(cases) if c["keep_log"]]
+    mode = N.MODE_AUTO if request.param == "auto" else N.MODE_GENERAL
     eng = BatchEngine(traces, cells, outcomes=True, log_cells=log_cells,
-                      log_steps=max_steps, log_ids=max_ids)
+                      log_steps=max_steps, log_ids=max_ids, mode=mode)
     eng.launch()
     res = eng.results()
     out = eng.outcomes()

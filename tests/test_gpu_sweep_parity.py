@@ -15,12 +15,15 @@ FIELDS = ("n_steps", "n_plans", "n_idle_skips", "request_steps", "completed", "c
           "tpot_violations")
 
 
-def test_sweep_grid_matches_oracle():
+@pytest.mark.parametrize("mode", ["auto", "general"])
+def test_sweep_grid_matches_oracle(mode):
     from oracle import oracle as orc
+    from paper_2505_23022_b200 import _native as N
     from paper_2505_23022_b200.batch import BatchEngine
 
     traces, cells = grid()
-    eng = BatchEngine(traces, cells, outcomes=True)
+    eng = BatchEngine(traces, cells, outcomes=True,
+                      mode=N.MODE_AUTO if mode == "auto" else N.MODE_GENERAL)
     eng.launch()
     res = eng.results()
     out = eng.outcomes()
