@@ -368,17 +368,13 @@ static void plan_baseline(sim_t* s, plan_t* pl) {
 }
 
 /* ------------------------------------------------------------------------ */
-static inline uint64_t fmix64(uint64_t k) {
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdULL;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ULL;
-  k ^= k >> 33;
-  return k;
-}
-
+/* digest item: mix(val ^ (step*K_STEP + tag*K_TAG + pos*K_POS)), mix(x) = y ^ (y >> 32)
+ * with y = x*K_MIX (all mod 2^64); the digest sums the items of all work steps. */
 uint64_t orc_digest_item(uint64_t step, uint32_t tag, uint32_t pos, uint64_t val) {
-  return fmix64(fmix64((step << 34) ^ ((uint64_t)tag << 32) ^ (uint64_t)pos) + val);
+  uint64_t key = step * 0x9E3779B97F4A7C15ULL + (uint64_t)tag * 0xC2B2AE3D27D4EB4FULL +
+                 (uint64_t)pos * 0x165667B19E3779F9ULL;
+  uint64_t y = (val ^ key) * 0xD6E8FEB86659FD93ULL;
+  return y ^ (y >> 32);
 }
 
 static uint64_t dbits(double x) {

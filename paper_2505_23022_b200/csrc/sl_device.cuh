@@ -163,18 +163,23 @@ __device__ __forceinline__ cred_t<WIDE> warp_min_cred(cred_t<WIDE> v) {
   return v;
 }
 
-// ---- work-step decision digest (oracle/scorpio_oracle.c orc_digest_item)
-__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdULL;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ULL;
-  k ^= k >> 33;
-  return k;
+// ---- work-step decision digest (oracle orc_digest_item).
+// item = mix(val ^ (step*K_STEP + tag*K_TAG + pos*K_POS)), mix(x) = (x*K_MIX) ^ ((x*K_MIX) >> 32);
+// the digest is the sum mod 2^64 of the items of all work steps.
+constexpr uint64_t kDigStep = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t kDigTag = 0xC2B2AE3D27D4EB4FULL;
+constexpr uint64_t kDigPos = 0x165667B19E3779F9ULL;
+constexpr uint64_t kDigMix = 0xD6E8FEB86659FD93ULL;
+__device__ __forceinline__ uint64_t digest_key(uint64_t step, uint32_t tag) {
+  return step * kDigStep + (uint64_t)tag * kDigTag;
+}
+__device__ __forceinline__ uint64_t digest_item_k(uint64_t key, uint32_t pos, uint64_t val) {
+  uint64_t x = (val ^ (key + (uint64_t)pos * kDigPos)) * kDigMix;
+  return x ^ (x >> 32);
 }
 __device__ __forceinline__ uint64_t digest_item(uint64_t step, uint32_t tag, uint32_t pos,
                                                 uint64_t val) {
-  return fmix64(fmix64((step << 34) ^ ((uint64_t)tag << 32) ^ (uint64_t)pos) + val);
+  return digest_item_k(digest_key(step, tag), pos, val);
 }
 
 }  // namespace sl

@@ -25,17 +25,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 M64 = (1 << 64) - 1
 
 
-def fmix64(k: int) -> int:
-    k ^= k >> 33
-    k = (k * 0xFF51AFD7ED558CCD) & M64
-    k ^= k >> 33
-    k = (k * 0xC4CEB9FE1A85EC53) & M64
-    k ^= k >> 33
-    return k
-
-
 def digest_item(step: int, tag: int, pos: int, val: int) -> int:
-    return fmix64((fmix64(((step << 34) ^ (tag << 32) ^ pos) & M64) + (val & M64)) & M64)
+    """Work-step digest item: mix(val ^ (step*K_STEP + tag*K_TAG + pos*K_POS))."""
+    key = (step * 0x9E3779B97F4A7C15 + tag * 0xC2B2AE3D27D4EB4F + pos * 0x165667B19E3779F9) & M64
+    y = (((val & M64) ^ key) * 0xD6E8FEB86659FD93) & M64
+    return y ^ (y >> 32)
 
 
 def dbits(x: float) -> int:
