@@ -341,6 +341,110 @@ __device__ __forceinline__ bool append_prefix(const Sim& s, const KArgs& a, int&
   return true;
 }
 
+// Retire entries whose last token was emitted at `end` (simengine.py:247-271):
+// outcomes, then stable compaction of the register slots through smem.
+template <bool WIDE>
+__device__ __forceinline__ void retire(const Sim& s, const KArgs& a, bool has_out,
+                                       Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
+                                       double end, int64_t step, Acc& acc, int lane,
+                                       Slot<WIDE>* scr) {
+  int q0 = 0;
+  unsigned retired_len = 0;
+#pragma unroll
+  for (int k = 0; k < kSlots; ++k) {
+    const int j = 32 * k + lane;
+    const bool ret = j < R && sl[k].rem <= 0;
+    const bool kp = j < R && !ret;
+    unsigned km = __ballot_sync(SL_FULL, kp);
+    if (kp) scr[q0 + __popc(km & lanemask_lt())] = sl[k];
+    q0 += __popc(km);
+    retired_len += __reduce_add_sync(SL_FULL, ret ? (unsigned)sl[k].cur_len : 0u);
+    if (ret) {
+      const int idx = sl[k].idx;
+      const WRec& w = s.wr[idx];
+      const double first = sl[k].first;
+      const int32_t tout = s.true_out[idx];
+      const double tpot = tout == 1 ? 0.0 : fdiv_(fsub_(end, first), (double)(tout - 1));
+      const double ttft = fsub_(first, w.arr);
+      const bool okc = ttft <= w.ttft && tpot <= w.tpot;
+      acc.completed++;
+      acc.compliant += okc;
+      acc.ttft_viol += ttft > w.ttft;
+      acc.tpot_viol += tpot > w.tpot;
+      if (has_out) {
+        const int64_t o = s.out_off + idx;
+        a.out.status[o] = SL_COMPLETED;
+        a.out.compliant[o] = okc;
+        a.out.completion_step[o] = (int32_t)step;
+        a.out.first_token_time[o] = first;
+        a.out.completion_time[o] = end;
+        a.out.ttft[o] = ttft;
+        a.out.tpot[o] = tpot;
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kSlots; ++k)
+    if (32 * k + lane < q0) sl[k] = scr[32 * k + lane];
+  __syncwarp();
+  R = q0;
+  g.lens -= retired_len;
+  g.inv_valid = false;
+  if (R > 0) {
+    g.Smin = running_min<WIDE>(sl, R, lane);
+    g.min_d = fixed_to_double<WIDE>(g.Smin, s.pow2E);
+  }
+}
+
+// Quiet steps: nothing waiting, no arrival due, <= 32 running, credit
+// batching, no decision log.  Exactly the general step restricted to that
+// case (no admission, so prefill_s is the empty sum 0 and now + 0 == now,
+// and the strictest entry always batches, so the step has work); kept as a
+// tight loop because these steps are the critical path of a sweep.
+template <bool WIDE>
+__device__ __forceinline__ void quiet_steps(const Sim& s, const KArgs& a, bool has_out,
+                                            Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
+                                            double& now, int64_t& step, int64_t& n_plans,
+                                            int64_t& req_steps, double next_t, bool has_h,
+                                            Acc& acc, int lane, Slot<WIDE>* scr) {
+  const sl_cost& C = s.cost;
+  const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
+  while (R > 0 && R <= 32 && next_t > now && now < horizon) {
+    ++n_plans;
+    req_steps += R;
+    // select_batch (sched_scorpio.py:171-179), fixed point
+    const bool live = lane < R;
+    const cred_t<WIDE> N = sl[0].N + g.Smin;
+    const bool b = live && N >= sl[0].S;
+    if (live) sl[0].N = b ? N - sl[0].S : N;
+    const unsigned bm = __ballot_sync(SL_FULL, b);
+    const int nb = __popc(bm);
+    // sum of current_len over the batch: butterfly over the live lanes only
+    unsigned v = b ? (unsigned)sl[0].cur_len : 0u;
+    for (int off = 1; off < R; off <<= 1) v += __shfl_xor_sync(SL_FULL, v, off);
+    const unsigned blen = __shfl_sync(SL_FULL, v, 0);
+    if (b) {
+      acc.dig += digest_item_k(digest_key((uint64_t)step, 2), __popc(bm & lanemask_lt()),
+                               (uint64_t)sl[0].id);
+      sl[0].cur_len += 1;
+      sl[0].rem -= 1;
+    }
+    g.lens += nb;
+    double L;
+    if ((nb & (nb - 1)) == 0)
+      L = fmul_((double)blen, __longlong_as_double((long long)(1023 - (__ffs(nb) - 1)) << 52));
+    else
+      L = fdiv_((double)blen, (double)nb);
+    const double end = fadd_(now, itl(C, nb, L));
+    if (lane == 0) acc.dig += digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
+    if (__any_sync(SL_FULL, live && sl[0].rem <= 0))
+      retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
+    now = end;
+    ++step;
+  }
+}
+
 template <bool WIDE>
 __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_out, int si, int lane,
                          Slot<WIDE>* scr) {
@@ -395,6 +499,11 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     if (next < n && next_t <= now)
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
+    if (W == 0 && credit && !logging && R > 0 && R <= 32) {
+      quiet_steps<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t, has_h, acc,
+                        lane, scr);
+      continue;
+    }
 
     ++n_plans;
     req_steps += W + R;
@@ -562,69 +671,23 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     }
 
     // ---- fresh entries emit their first token; retirement (simengine.py:240-271)
-    unsigned rmask[kSlots];
-    bool any_ret = false;
-#pragma unroll
-    for (int k = 0; k < kSlots; ++k) {
-      const int j = 32 * k + lane;
-      if (j >= R0 && j < R) {
-        sl[k].cur_len += 1;
-        sl[k].rem -= 1;
-        sl[k].first = end;
-      }
-      rmask[k] = __ballot_sync(SL_FULL, j < R && sl[k].rem <= 0);
-      any_ret |= rmask[k] != 0;
-    }
-    g.lens += nadm;
-    if (any_ret) {
-      int q0 = 0;
-      unsigned retired_len = 0;
+    if (nadm > 0) {
 #pragma unroll
       for (int k = 0; k < kSlots; ++k) {
         const int j = 32 * k + lane;
-        const bool ret = (rmask[k] >> lane) & 1u;
-        const bool kp = j < R && !ret;
-        unsigned km = __ballot_sync(SL_FULL, kp);
-        if (kp) scr[q0 + __popc(km & lanemask_lt())] = sl[k];
-        q0 += __popc(km);
-        retired_len += __reduce_add_sync(SL_FULL, ret ? (unsigned)sl[k].cur_len : 0u);
-        if (ret) {
-          const int idx = sl[k].idx;
-          const WRec& w = s.wr[idx];
-          const double first = sl[k].first;
-          const int32_t tout = s.true_out[idx];
-          const double tpot = tout == 1 ? 0.0 : fdiv_(fsub_(end, first), (double)(tout - 1));
-          const double ttft = fsub_(first, w.arr);
-          const bool okc = ttft <= w.ttft && tpot <= w.tpot;
-          acc.completed++;
-          acc.compliant += okc;
-          acc.ttft_viol += ttft > w.ttft;
-          acc.tpot_viol += tpot > w.tpot;
-          if (has_out) {
-            const int64_t o = s.out_off + idx;
-            a.out.status[o] = SL_COMPLETED;
-            a.out.compliant[o] = okc;
-            a.out.completion_step[o] = (int32_t)step;
-            a.out.first_token_time[o] = first;
-            a.out.completion_time[o] = end;
-            a.out.ttft[o] = ttft;
-            a.out.tpot[o] = tpot;
-          }
+        if (j >= R0 && j < R) {
+          sl[k].cur_len += 1;
+          sl[k].rem -= 1;
+          sl[k].first = end;
         }
       }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < kSlots; ++k)
-        if (32 * k + lane < q0) sl[k] = scr[32 * k + lane];
-      __syncwarp();
-      R = q0;
-      g.lens -= retired_len;
-      g.inv_valid = false;
-      if (R > 0) {
-        g.Smin = running_min<WIDE>(sl, R, lane);
-        g.min_d = fixed_to_double<WIDE>(g.Smin, s.pow2E);
-      }
+      g.lens += nadm;
     }
+    bool any_ret = false;
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k)
+      any_ret |= __any_sync(SL_FULL, 32 * k + lane < R && sl[k].rem <= 0);
+    if (any_ret) retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
     now = end;
     ++step;
   }

@@ -1,0 +1,4 @@
+# ncu captures: single critical-path sim and the full config-3 sweep (one launch each)
+timeout 300 ncu --set full --import-source on -k regex:sl_sim_fast -c 1 -o gpurun_out/prof_single python bench.py --rates 1 --scales 1 --steps 1 --warmup 1 --no-cpu > gpurun_out/prof_single.log 2>&1
+timeout 600 ncu --set full --import-source on -k regex:sl_sim_fast -c 1 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 1 --no-cpu > gpurun_out/prof_full.log 2>&1
+tail -1 gpurun_out/prof_full.log
