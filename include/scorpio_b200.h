@@ -180,9 +180,30 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
 /* Number of kernels sl_run_batch launches per call (for the gpu_launches claim). */
 int sl_run_batch_launches(void);
 
+/* ---- length predictor (LengthPredictor, predictor.py:93-126) ----------- */
+#define SL_PREDICT_ORACLE 0
+#define SL_PREDICT_NOISY_BUCKET 1
+
+typedef struct {
+  int32_t mode;         /* SL_PREDICT_* */
+  int32_t num_buckets;  /* Bucketing.num_buckets */
+  const double* boundaries; /* device, [num_buckets], strictly increasing */
+  double error_prob;
+  int32_t error_spread;
+  int32_t _pad;
+  uint64_t rng_seed;    /* default_rng([rng_seed, request.id]) */
+} sl_predictor;
+
+/* predicted_len for n requests (device arrays).  clamp_count (device, may be
+ * NULL) accumulates lengths above the last boundary (the reference logs a
+ * warning per clamp, predictor.py:75-81). */
+int sl_predict_batch(const int64_t* id, const int32_t* true_out, int64_t n,
+                     const sl_predictor* p, int32_t* out_pred, unsigned long long* clamp_count,
+                     void* stream);
+
 /* ABI self-description: writes sizeof(sl_sim), sizeof(sl_result),
- * sizeof(sl_traces), sizeof(sl_outcomes), sizeof(sl_log), sizeof(sl_cost)
- * into out[0..5] (n >= 6).  Lets bindings verify their struct mirrors. */
+ * sizeof(sl_traces), sizeof(sl_outcomes), sizeof(sl_log), sizeof(sl_cost),
+ * sizeof(sl_predictor) into out[0..6] (n >= 7).  Lets bindings verify their struct mirrors. */
 int sl_abi_layout(int64_t* out, int32_t n);
 
 /* Device properties used for grid sizing. */

@@ -83,6 +83,15 @@ class SlLog(C.Structure):
                                   "batch_ids", "n_steps")]
 
 
+class SlPredictor(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("num_buckets", C.c_int32), ("boundaries", C.c_void_p),
+                ("error_prob", C.c_double), ("error_spread", C.c_int32), ("_pad", C.c_int32),
+                ("rng_seed", C.c_uint64)]
+
+
+PREDICT_ORACLE, PREDICT_NOISY_BUCKET = 0, 1
+
+
 def build_native(verbose: bool = False) -> str:
     """Compile every CUDA source into lib/libscorpio_b200.so for sm_100a."""
     os.makedirs(LIB_DIR, exist_ok=True)
@@ -124,6 +133,9 @@ def lib():
     L.sl_abi_layout.restype = C.c_int
     L.sl_device_info.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.sl_device_info.restype = C.c_int
+    L.sl_predict_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(SlPredictor),
+                                   C.c_void_p, C.c_void_p, C.c_void_p]
+    L.sl_predict_batch.restype = C.c_int
     for name, args in _OPTIONAL_SIGS.items():
         if hasattr(L, name):
             fn = getattr(L, name)
@@ -138,11 +150,11 @@ _OPTIONAL_SIGS: dict = {}
 
 
 def _check_layout(L) -> None:
-    out = (C.c_int64 * 6)()
-    if L.sl_abi_layout(out, 6) != 0:
+    out = (C.c_int64 * 7)()
+    if L.sl_abi_layout(out, 7) != 0:
         raise NativeUnavailable("sl_abi_layout failed")
     want = (SIM_DTYPE.itemsize, RESULT_DTYPE.itemsize, C.sizeof(SlTraces), C.sizeof(SlOutcomes),
-            C.sizeof(SlLog), 8 * len(COST_FIELDS))
+            C.sizeof(SlLog), 8 * len(COST_FIELDS), C.sizeof(SlPredictor))
     if tuple(out) != want:
         raise NativeUnavailable(f"ABI layout mismatch: library {tuple(out)} vs binding {want}")
 

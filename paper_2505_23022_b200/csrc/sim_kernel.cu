@@ -650,13 +650,14 @@ int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_
 int sl_run_batch_launches(void) { return 2; }
 
 int sl_abi_layout(int64_t* out, int32_t n) {
-  if (!out || n < 6) return SL_ERR_ARG;
+  if (!out || n < 7) return SL_ERR_ARG;
   out[0] = sizeof(sl_sim);
   out[1] = sizeof(sl_result);
   out[2] = sizeof(sl_traces);
   out[3] = sizeof(sl_outcomes);
   out[4] = sizeof(sl_log);
   out[5] = sizeof(sl_cost);
+  out[6] = sizeof(sl_predictor);
   return SL_OK;
 }
 
