@@ -152,6 +152,13 @@ typedef struct {
   int32_t *n_admitted, *n_rejected, *n_batch;              /* [rows*step_cap] */
   int64_t *adm_ids, *rej_ids, *batch_ids;                  /* [rows*id_cap] */
   int64_t* n_steps; /* [rows] steps recorded */
+  double* adm_rec;  /* [rows*id_cap*5] may be NULL: AdmissionRecord (vbs, l_avg, min_slo,
+                       estimate, threshold) per admitted id of the scorpio TPOT guard */
+  int64_t skip_cap;
+  double* skip_now;     /* [rows*skip_cap] idle skips (EventLog.idle_skips) */
+  double* skip_target;  /* [rows*skip_cap] */
+  int32_t* skip_waiting; /* [rows*skip_cap] */
+  int64_t* n_skips;     /* [rows] */
 } sl_log;
 
 /* Workspace bytes for `total_slots` request slots (sum over sims of trace length). */
@@ -179,6 +186,84 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
 
 /* Number of kernels sl_run_batch launches per call (for the gpu_launches claim). */
 int sl_run_batch_launches(void);
+
+/* ---- batched plan_step over independent SchedulerStates ---------------
+ * (sched_scorpio.plan_step, sched_scorpio.py:210-316; config 2).  A batch is S
+ * "segments", each one SchedulerState (schedtypes.py:60-64): its waiting items
+ * in current queue order and its running entries in admission order. */
+#define SL_PLAN_WAITING 0
+#define SL_PLAN_REJECTED_TTFT 1
+#define SL_PLAN_REJECTED_ADMISSION 2
+#define SL_PLAN_ADMITTED 3
+#define SL_PLAN_GUARD_ONLY 64 /* flag: ttft_guard alone (no admission, sched_scorpio.py:183) */
+
+typedef struct {
+  int32_t n_segments;
+  int32_t _pad;
+  const int64_t* w_begin; /* [S+1] waiting-item ranges */
+  const int64_t* r_begin; /* [S+1] running-entry ranges */
+  /* waiting items (WaitingItem + its Request) */
+  const double* w_arrival;
+  const double* w_ttft;
+  const double* w_tpot;
+  const double* w_prefill; /* WaitingItem.prefill_s */
+  const int32_t* w_prompt;
+  const int32_t* w_pred; /* WaitingItem.predicted_len */
+  const int64_t* w_id;
+  /* running entries (RunningEntry) */
+  const double* r_tpot;
+  const int32_t* r_cur_len; /* prompt_len + tokens_generated */
+  const int64_t* r_id;
+  const uint64_t* r_credit; /* credit * tpot / 2^E (exact fixed point) */
+  const uint8_t* r_exclude; /* may be NULL: 1 = excluded from the credit phase */
+  /* per segment */
+  const double* now;         /* [S] SchedulerState.now */
+  const int32_t* credit_exp; /* [S] E (sl_credit_params over the segment's SLOs) */
+} sl_plan_state;
+
+typedef struct {
+  int32_t flags; /* SL_FLAG_TTFT_GUARD | SL_FLAG_TPOT_GUARD | SL_FLAG_R_ONLY | SL_PLAN_GUARD_ONLY */
+  int32_t _pad;
+  sl_cost cost;
+} sl_plan_config;
+
+typedef struct {
+  int32_t* perm;      /* [W] LDF order (global waiting indices), written by the sort */
+  int32_t* scratch;   /* [W] sort / walk scratch */
+  int32_t* adm_order; /* [W] admitted waiting indices in admission order (per segment) */
+  int32_t* w_status;  /* [W] SL_PLAN_* */
+  int32_t* w_pos;     /* [W] position in the new queue / in plan.rejected / admission order */
+  double* w_rec;      /* [W*5] may be NULL: AdmissionRecord vbs, l_avg, min_slo, estimate, threshold */
+  uint64_t* r_credit_out; /* [R] */
+  uint8_t* r_batch;       /* [R] 1 = in decode_batch */
+  int32_t* r_pos;         /* [R] position in decode_batch or -1 */
+  int32_t* seg_counts;    /* [S*4] waiting kept, admitted, rejected, batch */
+  uint64_t* seg_min_fixed; /* [S] min fixed-point slo over running + admitted (~0 if none) */
+  double* seg_vbs;        /* [S] plan.vbs */
+  double* seg_min_slo;    /* [S] plan.min_slo, NaN for None */
+} sl_plan_out;
+
+/* LDF sort of every segment's waiting queue by (deadline, arrival, id)
+ * (sched_scorpio.py:193).  max_w: host bound on any segment's size (selects the
+ * warp-bitonic, CTA-tile or tile+merge-path path). */
+int sl_ttft_sort_batch(const sl_plan_state* st, int64_t max_w, sl_plan_out* out, void* stream);
+/* TTFT walk + running aggregates + admission scan + vbs/min_slo per segment
+ * (sched_scorpio.py:196-294, 312-315).  Reads out->perm when TTFT_GUARD. */
+int sl_guard_admit_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_plan_out* out,
+                         void* stream);
+/* Credit phase select_batch (sched_scorpio.py:161-180), or decode-all when
+ * TPOT_GUARD is off.  The per-segment minimum comes from out->seg_min_fixed
+ * when use_seg_min (after sl_guard_admit_batch), else from the running entries. */
+int sl_credit_select_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_plan_out* out,
+                           int32_t use_seg_min, void* stream);
+/* plan_step over every segment: sort (if TTFT_GUARD) + guard/admit + select. */
+int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64_t max_w,
+                       sl_plan_out* out, void* stream);
+
+/* vbs(running, min_slo) (sched_scorpio.py:70-74) for S segments of running
+ * entries: Neumaier sum of min_slo[s] / tpot over each segment, in order. */
+int sl_vbs_batch(int32_t n_segments, const int64_t* r_begin, const double* r_tpot,
+                 const double* min_slo, double* out, void* stream);
 
 /* ---- length predictor (LengthPredictor, predictor.py:93-126) ----------- */
 #define SL_PREDICT_ORACLE 0

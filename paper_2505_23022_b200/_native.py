@@ -80,7 +80,37 @@ class SlLog(C.Structure):
     _fields_ = [("step_cap", C.c_int64), ("id_cap", C.c_int64)] + [
         (n, C.c_void_p) for n in ("now", "end", "prefill_s", "decode_s", "vbs", "min_slo",
                                   "n_admitted", "n_rejected", "n_batch", "adm_ids", "rej_ids",
-                                  "batch_ids", "n_steps")]
+                                  "batch_ids", "n_steps", "adm_rec")] + [
+        ("skip_cap", C.c_int64)] + [
+        (n, C.c_void_p) for n in ("skip_now", "skip_target", "skip_waiting", "n_skips")]
+
+
+class SlCost(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("alpha", "beta", "gamma", "delta", "epsilon", "phi",
+                                          "theta", "alpha_p", "beta_p")]
+
+
+class SlPlanState(C.Structure):
+    _fields_ = [("n_segments", C.c_int32), ("_pad", C.c_int32)] + [
+        (n, C.c_void_p) for n in ("w_begin", "r_begin", "w_arrival", "w_ttft", "w_tpot",
+                                  "w_prefill", "w_prompt", "w_pred", "w_id", "r_tpot",
+                                  "r_cur_len", "r_id", "r_credit", "r_exclude", "now",
+                                  "credit_exp")]
+
+
+class SlPlanConfig(C.Structure):
+    _fields_ = [("flags", C.c_int32), ("_pad", C.c_int32), ("cost", SlCost)]
+
+
+class SlPlanOut(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("perm", "scratch", "adm_order", "w_status", "w_pos",
+                                          "w_rec", "r_credit_out", "r_batch", "r_pos",
+                                          "seg_counts", "seg_min_fixed", "seg_vbs",
+                                          "seg_min_slo")]
+
+
+PLAN_WAITING, PLAN_REJECTED_TTFT, PLAN_REJECTED_ADMISSION, PLAN_ADMITTED = 0, 1, 2, 3
+PLAN_GUARD_ONLY = 64
 
 
 class SlPredictor(C.Structure):
@@ -136,6 +166,18 @@ def lib():
     L.sl_predict_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(SlPredictor),
                                    C.c_void_p, C.c_void_p, C.c_void_p]
     L.sl_predict_batch.restype = C.c_int
+    P = C.POINTER
+    L.sl_ttft_sort_batch.argtypes = [P(SlPlanState), C.c_int64, P(SlPlanOut), C.c_void_p]
+    L.sl_guard_admit_batch.argtypes = [P(SlPlanState), P(SlPlanConfig), P(SlPlanOut), C.c_void_p]
+    L.sl_credit_select_batch.argtypes = [P(SlPlanState), P(SlPlanConfig), P(SlPlanOut), C.c_int32,
+                                         C.c_void_p]
+    L.sl_plan_step_batch.argtypes = [P(SlPlanState), P(SlPlanConfig), C.c_int64, P(SlPlanOut),
+                                     C.c_void_p]
+    L.sl_vbs_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p]
+    for fn in ("sl_ttft_sort_batch", "sl_guard_admit_batch", "sl_credit_select_batch",
+               "sl_plan_step_batch", "sl_vbs_batch"):
+        getattr(L, fn).restype = C.c_int
     for name, args in _OPTIONAL_SIGS.items():
         if hasattr(L, name):
             fn = getattr(L, name)

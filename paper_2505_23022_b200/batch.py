@@ -169,7 +169,7 @@ class BatchEngine:
     def __init__(self, traces: list[TraceArrays], cells: list[Cell] | np.ndarray,
                  outcomes: bool = False, log_cells: list[int] | None = None,
                  log_steps: int = 0, log_ids: int = 0, order: np.ndarray | None = None,
-                 device=None, mode: int = N.MODE_AUTO):
+                 device=None, mode: int = N.MODE_AUTO, log_skips: int = 0):
         torch = N.require_cuda()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
@@ -234,10 +234,18 @@ class BatchEngine:
             for k in ("adm_ids", "rej_ids", "batch_ids"):
                 self._log[k] = torch.zeros(rows * ic, **i64)
             self._log["n_steps"] = torch.zeros(rows, **i64)
-            self.log_shape = (rows, sc, ic)
+            self._log["adm_rec"] = torch.zeros(rows * ic * 5, **f64)
+            kc = int(max(log_skips, 1))
+            self._log["skip_now"] = torch.zeros(rows * kc, **f64)
+            self._log["skip_target"] = torch.zeros(rows * kc, **f64)
+            self._log["skip_waiting"] = torch.zeros(rows * kc, **i32)
+            self._log["n_skips"] = torch.zeros(rows, **i64)
+            self.log_shape = (rows, sc, ic, kc)
             self.lg = N.SlLog(sc, ic, *[self._log[k].data_ptr() for k in (
                 "now", "end", "prefill_s", "decode_s", "vbs", "min_slo", "n_admitted",
-                "n_rejected", "n_batch", "adm_ids", "rej_ids", "batch_ids", "n_steps")])
+                "n_rejected", "n_batch", "adm_ids", "rej_ids", "batch_ids", "n_steps",
+                "adm_rec")], kc, *[self._log[k].data_ptr() for k in (
+                "skip_now", "skip_target", "skip_waiting", "n_skips")])
 
     def launch(self, stream=None) -> None:
         """One sl_run_batch on `stream` (default: torch's current stream)."""
@@ -276,7 +284,7 @@ class BatchEngine:
         row = int(self.sims_host[k]["log_slot"])
         if row < 0 or self.lg is None:
             raise RuntimeError("cell has no log slot")
-        rows, sc, ic = self.log_shape
+        rows, sc, ic, kc = self.log_shape
         ns = int(self._log["n_steps"][row].item())
         out = {f: self._log[f][row * sc: row * sc + ns].cpu().numpy() for f in (
             "now", "end", "prefill_s", "decode_s", "vbs", "min_slo", "n_admitted", "n_rejected",
@@ -285,6 +293,12 @@ class BatchEngine:
         out["adm_ids"] = self._log["adm_ids"][row * ic: row * ic + na].cpu().numpy()
         out["rej_ids"] = self._log["rej_ids"][row * ic: row * ic + nr].cpu().numpy()
         out["batch_ids"] = self._log["batch_ids"][row * ic: row * ic + nb].cpu().numpy()
+        out["adm_rec"] = self._log["adm_rec"][5 * row * ic: 5 * (row * ic + na)].cpu().numpy(
+        ).reshape(-1, 5)
+        nk = int(self._log["n_skips"][row].item())
+        out["skips"] = (self._log["skip_now"][row * kc: row * kc + nk].cpu().numpy(),
+                        self._log["skip_target"][row * kc: row * kc + nk].cpu().numpy(),
+                        self._log["skip_waiting"][row * kc: row * kc + nk].cpu().numpy())
         return out
 
 

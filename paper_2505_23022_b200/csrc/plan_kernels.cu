@@ -1,0 +1,557 @@
+// Batched plan_step over independent SchedulerStates (config 2 and the drop-in
+// sched_scorpio API): three separately launchable kernels.
+//
+//  sort   -- LDF order of each segment's waiting queue by (deadline, arrival,
+//            id) (sched_scorpio.py:193): warp bitonic network in registers for
+//            segments <= 32 items, CTA bitonic over shared memory for tiles of
+//            <= 2048, then merge-path passes between tiles for larger segments.
+//  guard  -- one warp per segment: speculative-parallel TTFT prefix walk,
+//            running aggregates (Neumaier 1/slo in running order), speculative
+//            greedy admission scan, then min_slo and vbs over running+admitted
+//            (sched_scorpio.py:196-294, 312-315).
+//  select -- one warp per segment: fixed-point credit earn/debit with ballot
+//            batch compaction (sched_scorpio.py:161-180), or decode-all.
+// All fp64 on the decision path uses the unfused *_rn intrinsics (sl_device.cuh).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "scorpio_b200.h"
+#include "sl_device.cuh"
+
+using namespace sl;
+
+namespace {
+
+constexpr int kTile = 2048;  // CTA sort tile
+constexpr int kSortThreads = 256;
+constexpr int kMergeItems = 4;  // outputs per thread in a merge pass
+
+struct Key {
+  double d, a;
+  int64_t id;
+  int32_t idx;
+};
+
+__device__ __forceinline__ bool key_lt(const Key& x, const Key& y) {
+  if (x.d != y.d) return x.d < y.d;
+  if (x.a != y.a) return x.a < y.a;
+  return x.id < y.id;
+}
+
+__device__ __forceinline__ Key load_key(const sl_plan_state& st, int32_t i) {
+  Key k;
+  k.a = st.w_arrival[i];
+  k.d = fadd_(k.a, st.w_ttft[i]);  // Request.deadline, core.py:50-53
+  k.id = st.w_id[i];
+  k.idx = i;
+  return k;
+}
+
+__device__ __forceinline__ Key inf_key() {
+  Key k;
+  k.d = __longlong_as_double(0x7ff0000000000000LL);
+  k.a = k.d;
+  k.id = INT64_MAX;
+  k.idx = -1;
+  return k;
+}
+
+// ---- sort: one warp per segment (<= 32 items), bitonic network over shuffles
+__global__ void sort_warp_kernel(const sl_plan_state st, int32_t* perm) {
+  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= st.n_segments) return;
+  const int64_t b = st.w_begin[seg];
+  const int n = (int)(st.w_begin[seg + 1] - b);
+  Key k = lane < n ? load_key(st, (int32_t)(b + lane)) : inf_key();
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      Key o;
+      o.d = __shfl_xor_sync(SL_FULL, k.d, j);
+      o.a = __shfl_xor_sync(SL_FULL, k.a, j);
+      o.id = __shfl_xor_sync(SL_FULL, k.id, j);
+      o.idx = __shfl_xor_sync(SL_FULL, k.idx, j);
+      const bool up = (lane & size) == 0;
+      const bool lower = (lane & j) == 0;
+      const bool take = (lower == up) ? key_lt(o, k) : key_lt(k, o);
+      if (take) k = o;
+    }
+  }
+  if (lane < n) perm[b + lane] = k.idx;
+}
+
+// ---- sort: one CTA per (segment, tile of <= kTile items), bitonic over smem
+__global__ void __launch_bounds__(kSortThreads) sort_tile_kernel(const sl_plan_state st,
+                                                                 int tiles_per_seg, int32_t* out) {
+  extern __shared__ unsigned char smem_raw[];
+  double* sd = reinterpret_cast<double*>(smem_raw);
+  double* sa = sd + kTile;
+  int64_t* sid = reinterpret_cast<int64_t*>(sa + kTile);
+  int32_t* sidx = reinterpret_cast<int32_t*>(sid + kTile);
+  const int seg = blockIdx.x / tiles_per_seg;
+  const int tile = blockIdx.x % tiles_per_seg;
+  const int64_t sb = st.w_begin[seg], se = st.w_begin[seg + 1];
+  const int64_t b = sb + (int64_t)tile * kTile;
+  if (b >= se) return;
+  const int n = (int)min((int64_t)kTile, se - b);
+  int P = 32;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    Key k = i < n ? load_key(st, (int32_t)(b + i)) : inf_key();
+    sd[i] = k.d;
+    sa[i] = k.a;
+    sid[i] = k.id;
+    sidx[i] = k.idx;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+        const int lo = 2 * j * (t / j) + (t % j);
+        const int hi = lo + j;
+        const bool up = (lo & size) == 0;
+        Key x{sd[lo], sa[lo], sid[lo], sidx[lo]};
+        Key y{sd[hi], sa[hi], sid[hi], sidx[hi]};
+        const bool swap = up ? key_lt(y, x) : key_lt(x, y);
+        if (swap) {
+          sd[lo] = y.d; sa[lo] = y.a; sid[lo] = y.id; sidx[lo] = y.idx;
+          sd[hi] = x.d; sa[hi] = x.a; sid[hi] = x.id; sidx[hi] = x.idx;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[b + i] = sidx[i];
+}
+
+// ---- sort: merge-path pass over runs of width w inside each segment
+__global__ void merge_pass_kernel(const sl_plan_state st, int64_t w, int blocks_per_seg,
+                                  const int32_t* __restrict__ src, int32_t* __restrict__ dst) {
+  const int seg = blockIdx.x / blocks_per_seg;
+  const int64_t sb = st.w_begin[seg], se = st.w_begin[seg + 1];
+  const int64_t p0 = ((int64_t)(blockIdx.x % blocks_per_seg) * blockDim.x + threadIdx.x) *
+                     kMergeItems;  // output offset inside the segment
+  const int64_t n = se - sb;
+  if (p0 >= n) return;
+  const int64_t pair = p0 / (2 * w);
+  const int64_t base = sb + pair * 2 * w;
+  const int64_t la = min(w, se - base);
+  const int64_t lb = max((int64_t)0, min(w, se - base - w));
+  const int32_t* A = src + base;
+  const int32_t* B = src + base + w;
+  const int64_t q = p0 - pair * 2 * w;  // diagonal inside the pair
+  // merge path: first i with A[i] > B[q-i-1] (A wins ties; keys are unique)
+  int64_t lo = max((int64_t)0, q - lb), hi = min(q, la);
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key_lt(load_key(st, B[q - mid - 1]), load_key(st, A[mid])))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  int64_t i = lo, j = q - lo;
+  for (int t = 0; t < kMergeItems && q + t < la + lb; ++t) {
+    bool takeA;
+    if (i >= la)
+      takeA = false;
+    else if (j >= lb)
+      takeA = true;
+    else
+      takeA = !key_lt(load_key(st, B[j]), load_key(st, A[i]));
+    dst[base + q + t] = takeA ? A[i++] : B[j++];
+  }
+}
+
+__global__ void copy_kernel(const sl_plan_state st, const int32_t* __restrict__ src,
+                            int32_t* __restrict__ dst) {
+  const int64_t n = st.w_begin[st.n_segments] - st.w_begin[0];
+  src += st.w_begin[0];
+  dst += st.w_begin[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// ---- guard + admission: one warp per segment
+__global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config cfg,
+                                   sl_plan_out out) {
+  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= st.n_segments) return;
+  const sl_cost& C = cfg.cost;
+  const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
+  const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
+  const bool r_only = cfg.flags & SL_FLAG_R_ONLY;
+  const bool guard_only = cfg.flags & SL_PLAN_GUARD_ONLY;
+  const int64_t wb = st.w_begin[seg], rb = st.r_begin[seg];
+  const int W = (int)(st.w_begin[seg + 1] - wb);
+  const int R = (int)(st.r_begin[seg + 1] - rb);
+  const double now = st.now[seg];
+  const int E = st.credit_exp[seg];
+  const double pow2E = __longlong_as_double((long long)(E + 1023) << 52);
+  int32_t* kept_list = out.scratch + wb;
+  int nrej = 0, kept = 0;
+
+  // 1. TTFT walk over the LDF order (speculative-parallel, exact), or the FCFS queue
+  {
+    double prefix = 0.0;
+    for (int c0 = 0; c0 < W; c0 += 32) {
+      const int p = c0 + lane;
+      const bool valid = p < W;
+      const int cnt = min(32, W - c0);
+      int32_t idx = 0;
+      double e = 0.0, pf = 0.0, tt = 0.0;
+      if (valid) {
+        idx = ttft_guard ? out.perm[wb + p] : (int32_t)(wb + p);
+        e = fsub_(now, st.w_arrival[idx]);
+        pf = st.w_prefill[idx];
+        tt = st.w_ttft[idx];
+      }
+      unsigned rejm = 0;
+      if (ttft_guard) {
+        int start = 0;
+        while (start < cnt) {
+          double run = prefix, mine = 0.0;
+          for (int t = start; t < cnt; ++t) {
+            const double x = bcast(pf, t);
+            if (lane == t) mine = run;
+            run = fadd_(run, x);
+          }
+          const bool rj = lane >= start && lane < cnt && fadd_(fadd_(e, mine), pf) > tt;
+          const unsigned m = __ballot_sync(SL_FULL, rj);
+          if (m == 0) {
+            prefix = run;
+            break;
+          }
+          const int r = __ffs(m) - 1;
+          rejm |= 1u << r;
+          prefix = bcast(mine, r);
+          start = r + 1;
+        }
+      }
+      const bool rj = valid && ((rejm >> lane) & 1u);
+      const bool keep = valid && !rj;
+      const unsigned km = __ballot_sync(SL_FULL, keep);
+      if (keep) kept_list[kept + __popc(km & lanemask_lt())] = idx;
+      if (rj) {
+        out.w_status[idx] = SL_PLAN_REJECTED_TTFT;
+        out.w_pos[idx] = nrej + __popc(rejm & lanemask_lt());
+      }
+      kept += __popc(km);
+      nrej += __popc(rejm);
+    }
+    __syncwarp();
+  }
+  if (guard_only) {
+    for (int p = lane; p < kept; p += 32) {
+      out.w_status[kept_list[p]] = SL_PLAN_WAITING;
+      out.w_pos[kept_list[p]] = p;
+    }
+    if (lane == 0) {
+      out.seg_counts[4 * seg + 0] = kept;
+      out.seg_counts[4 * seg + 1] = 0;
+      out.seg_counts[4 * seg + 2] = nrej;
+    }
+    return;
+  }
+
+  // 2. running aggregates (sched_scorpio.py:117-124)
+  int64_t lens = 0;
+  double min_d = __longlong_as_double(0x7ff0000000000000LL);
+  for (int j = lane; j < R; j += 32) {
+    lens += st.r_cur_len[rb + j];
+    min_d = fmin(min_d, st.r_tpot[rb + j]);
+  }
+  lens = warp_sum_i64(lens);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) min_d = fmin(min_d, __shfl_xor_sync(SL_FULL, min_d, o));
+  bool has_min = R > 0;
+  int nadm = 0, nwait = 0;
+  int32_t* adm = out.adm_order + wb;
+
+  if (tpot_guard) {
+    double inv = 0.0;
+    if (kept > 0) {
+      PySum ps;
+      ps_init(ps);
+      for (int c0 = 0; c0 < R; c0 += 32) {
+        const int j = c0 + lane;
+        const double x = j < R ? fdiv_(1.0, st.r_tpot[rb + j]) : 0.0;
+        const int cnt = min(32, R - c0);
+        for (int t = 0; t < cnt; ++t) ps_add(ps, bcast(x, t));
+      }
+      inv = ps_result(ps);
+    }
+    int64_t n_run = R;
+    // 3. admission scan, speculative-parallel (sched_scorpio.py:237-294)
+    for (int c0 = 0; c0 < kept; c0 += 32) {
+      const int p = c0 + lane;
+      const bool valid = p < kept;
+      int32_t idx = 0, ln = 0, pred = 0;
+      double tp = 1.0, ic = 0.0;
+      if (valid) {
+        idx = kept_list[p];
+        tp = st.w_tpot[idx];
+        ic = fdiv_(1.0, tp);
+        ln = st.w_prompt[idx];
+        pred = st.w_pred[idx];
+      }
+      // feasible alone? (solo test, :279-289)
+      const bool solo = solo_ok(C, tp, ic, ln, pred);
+      unsigned pend = __ballot_sync(SL_FULL, valid);
+      while (pend) {
+        const bool lt = !has_min || tp < min_d;
+        const double minp = lt ? tp : min_d;
+        const double V = fmul_(minp, fadd_(inv, ic));
+        const double L = fdiv_((double)(lens + ln), (double)(n_run + 1));
+        const double est = tpot_estimate(C, V, L, pred);
+        const double thr = (r_only && has_min) ? min_d : minp;
+        const bool ok = ((pend >> lane) & 1u) && est <= thr;
+        const unsigned okm = __ballot_sync(SL_FULL, ok);
+        const int g = okm ? __ffs(okm) - 1 : 32;
+        const unsigned fail = okm ? (pend & ((1u << g) - 1u)) : pend;
+        const bool mf = (fail >> lane) & 1u;
+        const bool keep = mf && solo;
+        const bool rj = mf && !solo;
+        const unsigned km = __ballot_sync(SL_FULL, keep);
+        const unsigned rm = __ballot_sync(SL_FULL, rj);
+        if (keep) {
+          out.w_status[idx] = SL_PLAN_WAITING;
+          out.w_pos[idx] = nwait + __popc(km & lanemask_lt());
+        }
+        if (rj) {
+          out.w_status[idx] = SL_PLAN_REJECTED_ADMISSION;
+          out.w_pos[idx] = nrej + __popc(rm & lanemask_lt());
+        }
+        nwait += __popc(km);
+        nrej += __popc(rm);
+        pend &= ~fail;
+        if (!okm) break;
+        if (lane == g) {
+          out.w_status[idx] = SL_PLAN_ADMITTED;
+          out.w_pos[idx] = nadm;
+          adm[nadm] = idx;
+          if (out.w_rec) {
+            double* r5 = out.w_rec + 5 * (int64_t)idx;
+            r5[0] = V;
+            r5[1] = L;
+            r5[2] = minp;
+            r5[3] = est;
+            r5[4] = thr;
+          }
+        }
+        // state update (:272-277)
+        const double tp_g = bcast(tp, g);
+        n_run += 1;
+        inv = fadd_(inv, bcast(ic, g));
+        lens += bcast(ln, g);
+        if (!has_min || tp_g < min_d) min_d = tp_g;
+        has_min = true;
+        ++nadm;
+        pend &= ~(1u << g);
+      }
+    }
+  } else {  // admit everything in queue order (:295-304)
+    for (int p = lane; p < kept; p += 32) {
+      const int32_t idx = kept_list[p];
+      out.w_status[idx] = SL_PLAN_ADMITTED;
+      out.w_pos[idx] = p;
+      adm[p] = idx;
+    }
+    for (int c0 = 0; c0 < kept; c0 += 32) {
+      const int p = c0 + lane;
+      double v = p < kept ? st.w_tpot[kept_list[p]] : min_d;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(SL_FULL, v, o));
+      min_d = fmin(min_d, v);
+    }
+    has_min = has_min || kept > 0;
+    nadm = kept;
+  }
+  __syncwarp();
+
+  // 4. plan.min_slo / plan.vbs over running + admitted, in order (:312-315)
+  double vbs = 0.0;
+  if (has_min) {
+    PySum vs;
+    ps_init(vs);
+    const int tot = R + nadm;
+    for (int c0 = 0; c0 < tot; c0 += 32) {
+      const int j = c0 + lane;
+      double x = 0.0;
+      if (j < tot) x = fdiv_(min_d, j < R ? st.r_tpot[rb + j] : st.w_tpot[adm[j - R]]);
+      const int cnt = min(32, tot - c0);
+      for (int t = 0; t < cnt; ++t) ps_add(vs, bcast(x, t));
+    }
+    vbs = ps_result(vs);
+  }
+  if (lane == 0) {
+    out.seg_counts[4 * seg + 0] = nwait;
+    out.seg_counts[4 * seg + 1] = nadm;
+    out.seg_counts[4 * seg + 2] = nrej;
+    out.seg_vbs[seg] = vbs;
+    out.seg_min_slo[seg] = has_min ? min_d : __longlong_as_double(0x7ff8000000000000LL);
+    out.seg_min_fixed[seg] = has_min ? slo_fixed<false>(min_d, E) : ~0ull;
+  }
+  (void)pow2E;
+}
+
+// ---- credit select / decode-all: one warp per segment
+__global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_config cfg,
+                                     sl_plan_out out, int use_seg_min) {
+  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= st.n_segments) return;
+  const bool credit = cfg.flags & SL_FLAG_TPOT_GUARD;
+  const int64_t rb = st.r_begin[seg];
+  const int R = (int)(st.r_begin[seg + 1] - rb);
+  const int E = st.credit_exp[seg];
+  uint64_t MIN = ~0ull;
+  if (credit) {
+    if (use_seg_min) {
+      MIN = out.seg_min_fixed[seg];
+    } else {
+      for (int j = lane; j < R; j += 32) {
+        const uint64_t S = slo_fixed<false>(st.r_tpot[rb + j], E);
+        MIN = S < MIN ? S : MIN;
+      }
+      MIN = warp_min_cred<false>(MIN);
+    }
+  }
+  int nb = 0;
+  for (int c0 = 0; c0 < R; c0 += 32) {
+    const int j = c0 + lane;
+    bool b = false;
+    if (j < R) {
+      const int64_t r = rb + j;
+      const bool ex = st.r_exclude && st.r_exclude[r];
+      uint64_t N = st.r_credit[r];
+      if (!ex) {
+        if (credit) {
+          const uint64_t S = slo_fixed<false>(st.r_tpot[r], E);
+          N += MIN;
+          b = N >= S;
+          if (b) N -= S;
+        } else {
+          b = true;
+        }
+      }
+      out.r_credit_out[r] = N;
+    }
+    const unsigned bm = __ballot_sync(SL_FULL, b);
+    if (j < R) {
+      out.r_batch[rb + j] = b;
+      out.r_pos[rb + j] = b ? nb + __popc(bm & lanemask_lt()) : -1;
+    }
+    nb += __popc(bm);
+  }
+  if (lane == 0) out.seg_counts[4 * seg + 3] = nb;
+}
+
+__global__ void vbs_kernel(int S, const int64_t* r_begin, const double* r_tpot,
+                           const double* min_slo, double* out) {
+  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= S) return;
+  const int64_t rb = r_begin[seg];
+  const int R = (int)(r_begin[seg + 1] - rb);
+  const double m = min_slo[seg];
+  PySum vs;
+  ps_init(vs);
+  for (int c0 = 0; c0 < R; c0 += 32) {
+    const int j = c0 + lane;
+    const double x = j < R ? fdiv_(m, r_tpot[rb + j]) : 0.0;  // trp, :63-67
+    const int cnt = min(32, R - c0);
+    for (int t = 0; t < cnt; ++t) ps_add(vs, bcast(x, t));
+  }
+  if (lane == 0) out[seg] = ps_result(vs);  // empty -> 0.0 (:72-73)
+}
+
+int warps_grid(int n_warps, int threads) { return (n_warps * 32 + threads - 1) / threads; }
+
+}  // namespace
+
+extern "C" {
+
+int sl_ttft_sort_batch(const sl_plan_state* st, int64_t max_w, sl_plan_out* out, void* stream) {
+  if (!st || !out || !out->perm || max_w < 0) return SL_ERR_ARG;
+  const int S = st->n_segments;
+  if (S == 0 || max_w == 0) return SL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (max_w <= 32) {
+    sort_warp_kernel<<<warps_grid(S, 128), 128, 0, s>>>(*st, out->perm);
+    return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+  }
+  if (!out->scratch) return SL_ERR_ARG;
+  const int tiles = (int)((max_w + kTile - 1) / kTile);
+  const size_t smem = (size_t)kTile * (8 + 8 + 8 + 4);
+  cudaFuncSetAttribute(sort_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  sort_tile_kernel<<<S * tiles, kSortThreads, smem, s>>>(*st, tiles, out->perm);
+  int32_t* src = out->perm;
+  int32_t* dst = out->scratch;
+  for (int64_t w = kTile; w < max_w; w *= 2) {
+    const int per_block = 256 * kMergeItems;
+    const int bps = (int)((max_w + per_block - 1) / per_block);
+    merge_pass_kernel<<<S * bps, 256, 0, s>>>(*st, w, bps, src, dst);
+    int32_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  if (src != out->perm) {
+    copy_kernel<<<592, 256, 0, s>>>(*st, src, out->perm);
+  }
+  return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+}
+
+int sl_guard_admit_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_plan_out* out,
+                         void* stream) {
+  if (!st || !cfg || !out || !out->scratch || !out->w_status || !out->w_pos || !out->seg_counts)
+    return SL_ERR_ARG;
+  if (!(cfg->flags & SL_PLAN_GUARD_ONLY) &&
+      (!out->adm_order || !out->seg_vbs || !out->seg_min_slo || !out->seg_min_fixed))
+    return SL_ERR_ARG;
+  if ((cfg->flags & SL_FLAG_TTFT_GUARD) && !out->perm) return SL_ERR_ARG;
+  if (st->n_segments == 0) return SL_OK;
+  guard_admit_kernel<<<warps_grid(st->n_segments, 128), 128, 0, (cudaStream_t)stream>>>(*st, *cfg,
+                                                                                        *out);
+  return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+}
+
+int sl_credit_select_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_plan_out* out,
+                           int32_t use_seg_min, void* stream) {
+  if (!st || !cfg || !out || !out->r_credit_out || !out->r_batch || !out->r_pos ||
+      !out->seg_counts || (use_seg_min && !out->seg_min_fixed))
+    return SL_ERR_ARG;
+  if (st->n_segments == 0) return SL_OK;
+  credit_select_kernel<<<warps_grid(st->n_segments, 128), 128, 0, (cudaStream_t)stream>>>(
+      *st, *cfg, *out, use_seg_min);
+  return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+}
+
+int sl_vbs_batch(int32_t n_segments, const int64_t* r_begin, const double* r_tpot,
+                 const double* min_slo, double* out, void* stream) {
+  if (n_segments < 0 || (n_segments > 0 && (!r_begin || !min_slo || !out))) return SL_ERR_ARG;
+  if (n_segments == 0) return SL_OK;
+  vbs_kernel<<<warps_grid(n_segments, 128), 128, 0, (cudaStream_t)stream>>>(n_segments, r_begin,
+                                                                           r_tpot, min_slo, out);
+  return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+}
+
+int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64_t max_w,
+                       sl_plan_out* out, void* stream) {
+  if (!st || !cfg || !out) return SL_ERR_ARG;
+  int rc;
+  if (cfg->flags & SL_FLAG_TTFT_GUARD) {
+    rc = sl_ttft_sort_batch(st, max_w, out, stream);
+    if (rc) return rc;
+  }
+  rc = sl_guard_admit_batch(st, cfg, out, stream);
+  if (rc) return rc;
+  if (cfg->flags & SL_PLAN_GUARD_ONLY) return SL_OK;
+  return sl_credit_select_batch(st, cfg, out, 1, stream);
+}
+
+}  // extern "C"

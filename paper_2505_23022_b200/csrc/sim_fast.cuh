@@ -241,6 +241,18 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       const double pf_g = bcast(pf, gl);
       const bool lt_g = bcast((int)lt, gl) != 0;
       put_slot<WIDE>(sl, R, e, lane);
+      if (lg_adm >= 0 && a.log.adm_rec) {  // AdmissionRecord inputs (sched_scorpio.py:254-271)
+        const double r0 = bcast(V, gl), r1 = bcast(L, gl), r2 = bcast(minp, gl);
+        const double r3 = bcast(est, gl), r4 = bcast(thr, gl);
+        if (lane == 0 && nadm < cap_adm) {
+          double* rec = a.log.adm_rec + 5 * (lg_adm + nadm);
+          rec[0] = r0;
+          rec[1] = r1;
+          rec[2] = r2;
+          rec[3] = r3;
+          rec[4] = r4;
+        }
+      }
       if (lane == 0) {
         acc.dig += digest_item((uint64_t)step, 0, (uint32_t)nadm, (uint64_t)e.id);
         if (lg_adm >= 0 && nadm < cap_adm) a.log.adm_ids[lg_adm + nadm] = e.id;
@@ -608,6 +620,15 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       if (target <= now) {
         status = SL_SIM_NO_PROGRESS;
         break;
+      }
+      if (logging && a.log.skip_now && lane == 0) {  // EventLog.idle_skips (simengine.py:225)
+        if (n_idle < a.log.skip_cap) {
+          const int64_t o = s.log_row * a.log.skip_cap + n_idle;
+          a.log.skip_now[o] = now;
+          a.log.skip_target[o] = target;
+          a.log.skip_waiting[o] = W;
+          a.log.n_skips[s.log_row] = n_idle + 1;
+        }
       }
       ++n_idle;
       now = target;

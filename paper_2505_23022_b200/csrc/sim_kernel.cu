@@ -301,6 +301,17 @@ __device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_inde
               double est = tpot_estimate(C, V, L, cpred);
               double thr = (r_only && has_min) ? min_d : minp;
               if (est <= thr) {
+                if (lg_adm >= 0 && a.log.adm_rec && lane == 0) {  // AdmissionRecord inputs
+                  const int q = nadm + __popc(adm);
+                  if (q < cap_adm) {
+                    double* rec = a.log.adm_rec + 5 * (lg_adm + q);
+                    rec[0] = V;
+                    rec[1] = L;
+                    rec[2] = minp;
+                    rec[3] = est;
+                    rec[4] = thr;
+                  }
+                }
                 adm |= 1u << t;
                 n_run += 1;
                 inv = fadd_(inv, icand);  // plain float add, :275
@@ -441,6 +452,13 @@ __device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_inde
       if (target <= now) {
         status = SL_SIM_NO_PROGRESS;
         break;
+      }
+      if (logging && a.log.skip_now && lane == 0 && n_idle < a.log.skip_cap) {
+        const int64_t o = s.log_row * a.log.skip_cap + n_idle;
+        a.log.skip_now[o] = now;
+        a.log.skip_target[o] = target;
+        a.log.skip_waiting[o] = W;
+        a.log.n_skips[s.log_row] = n_idle + 1;
       }
       n_idle++;
       now = target;

@@ -1,0 +1,98 @@
+"""Seeded scheduler-state snapshots for config 2: S independent
+SchedulerStates ("segments") with W waiting and R running requests each.
+
+Tiers as config 1 (TTFT/TPOT (0.5 s, 30 ms), (2.0 s, 50 ms), (7.5 s, 100 ms)),
+arrivals U[now - 0.4, now], prompt U[20, 600], output U[5, 400], tokens
+U[1, output), credits reachable fixed-point values (k * MIN mod S, i.e. the
+credit after k credit phases).  Arrays only (numpy), so the same snapshot can be
+materialised as objects of either the reference or this package.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+TIERS = ((0.5, 0.030), (2.0, 0.050), (7.5, 0.100))
+ACC_PREFILL = (0.004, 128.0, 2e-5, 1.5e-3)
+
+
+def _prefill(phi, theta, ap, bp, n):
+    return phi if n <= theta else ap * n + bp
+
+
+def config2_arrays(n_segments: int, w: int, r: int, seed: int, now: float = 10.0,
+                   prefill=ACC_PREFILL) -> dict[str, np.ndarray]:
+    rng = np.random.default_rng(seed)
+    S, W, R = n_segments, n_segments * w, n_segments * r
+    tier_w = rng.integers(0, 3, W)
+    tier_r = rng.integers(0, 3, R)
+    out_w = rng.integers(5, 401, W)
+    out_r = rng.integers(5, 401, R)
+    a = {
+        "w_begin": np.arange(S + 1, dtype=np.int64) * w,
+        "r_begin": np.arange(S + 1, dtype=np.int64) * r,
+        "w_id": np.arange(W, dtype=np.int64),
+        "w_arrival": now - rng.uniform(0.0, 0.4, W),
+        "w_ttft": np.array([TIERS[t][0] for t in tier_w]),
+        "w_tpot": np.array([TIERS[t][1] for t in tier_w]),
+        "w_prompt": rng.integers(20, 601, W).astype(np.int32),
+        "w_pred": out_w.astype(np.int32),
+        "r_id": np.arange(W, W + R, dtype=np.int64),
+        "r_tpot": np.array([TIERS[t][1] for t in tier_r]),
+        "r_prompt": rng.integers(20, 601, R).astype(np.int32),
+        "r_out": out_r.astype(np.int32),
+        "r_tokens": np.array([int(rng.integers(1, o)) for o in out_r], np.int32),
+        "r_k": rng.integers(0, 1000, R),
+        "now": np.full(S, now),
+    }
+    a["w_prefill"] = np.array([_prefill(*prefill, int(n)) for n in a["w_prompt"]])
+    # credit numerators: after k phases at the strictest tier, (k * MIN) mod S_e
+    E = min(math.frexp(t)[1] for _, t in TIERS) - 53
+    smin = int(np.ldexp(TIERS[0][1], -E))
+    a["r_credit_num"] = np.array(
+        [(int(k) * smin) % int(np.ldexp(t, -E)) for k, t in zip(a["r_k"], a["r_tpot"])],
+        dtype=object)
+    a["credit_exp"] = np.full(S, E, np.int32)
+    return a
+
+
+def plan_arrays(a: dict) -> dict[str, np.ndarray]:
+    """The sl_plan_state SoA (PlanBatch(arrays=...)) of a snapshot, no objects."""
+    out = {k: a[k] for k in ("w_begin", "r_begin", "w_arrival", "w_ttft", "w_tpot", "w_prefill",
+                             "w_prompt", "w_pred", "w_id", "r_tpot", "r_id", "now", "credit_exp")}
+    out["r_cur_len"] = (a["r_prompt"] + a["r_tokens"]).astype(np.int32)
+    out["r_credit"] = np.array([int(x) for x in a["r_credit_num"]], np.uint64)
+    return out
+
+
+def states_from_arrays(a: dict, types) -> list:
+    """Materialise SchedulerState objects with `types` = module-like object with
+    Request, WaitingItem, RunningEntry, SchedulerState (reference or drop-in)."""
+    from fractions import Fraction
+
+    S = len(a["now"])
+    out = []
+    E = int(a["credit_exp"][0])
+    for s in range(S):
+        st = types.SchedulerState(now=float(a["now"][s]))
+        for i in range(int(a["w_begin"][s]), int(a["w_begin"][s + 1])):
+            req = types.Request(id=int(a["w_id"][i]), arrival_time=float(a["w_arrival"][i]),
+                                prompt_len=int(a["w_prompt"][i]),
+                                true_output_len=int(a["w_pred"][i]),
+                                ttft_slo=float(a["w_ttft"][i]), tpot_slo=float(a["w_tpot"][i]))
+            st.waiting.append(types.WaitingItem(request=req, predicted_len=int(a["w_pred"][i]),
+                                                prefill_s=float(a["w_prefill"][i])))
+        for j in range(int(a["r_begin"][s]), int(a["r_begin"][s + 1])):
+            req = types.Request(id=int(a["r_id"][j]), arrival_time=0.0,
+                                prompt_len=int(a["r_prompt"][j]),
+                                true_output_len=int(a["r_out"][j]), ttft_slo=1.0,
+                                tpot_slo=float(a["r_tpot"][j]))
+            e = types.RunningEntry(request=req, predicted_len=int(a["r_out"][j]), prefill_s=0.0)
+            e.tokens_generated = int(a["r_tokens"][j])
+            e.credit = Fraction(int(a["r_credit_num"][j])) * Fraction(2) ** E / \
+                Fraction(float(a["r_tpot"][j]))
+            st.running.append(e)
+        out.append(st)
+    return out

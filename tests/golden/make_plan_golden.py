@@ -1,0 +1,86 @@
+"""Reference plan_step outputs on seeded config-2 snapshots (run in the build
+container, where /root/reference exists).  Inputs are regenerated from seeds by
+paper_2505_23022_b200.snapshot on the GPU box; only outputs are stored.
+
+    python tests/golden/make_plan_golden.py
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import types
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+CASES = [  # (name, segments, W, R, seed, flags)
+    ("primary_32x32", 64, 32, 32, 1, "both"),
+    ("small_mixed", 96, 7, 5, 2, "both"),
+    ("mid_300x60", 8, 300, 60, 3, "both"),
+    ("r_only", 32, 32, 32, 4, "r_only"),
+    ("ttft_only", 32, 32, 32, 5, "ttft_only"),
+    ("tpot_only", 32, 32, 32, 6, "tpot_only"),
+    ("neither", 16, 32, 32, 7, "neither"),
+    ("tile_merge_5000", 1, 5000, 300, 8, "both"),
+    ("stress_32768", 1, 32768, 32768, 9, "both"),
+]
+
+
+def main() -> None:
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, "/root/reference/pkg/src")
+    sys.path.insert(0, ROOT)
+    from slosim import core, schedtypes
+    from slosim.costmodel import ItlParams, PrefillParams
+    from slosim.predictor import Bucketing, LengthPredictor
+    from slosim.sched_scorpio import ScorpioConfig, plan_step
+
+    from paper_2505_23022_b200.snapshot import config2_arrays, states_from_arrays
+
+    T = types.SimpleNamespace(Request=core.Request, WaitingItem=schedtypes.WaitingItem,
+                              RunningEntry=schedtypes.RunningEntry,
+                              SchedulerState=schedtypes.SchedulerState)
+    itl = ItlParams(1e-6, 1e-3, 1e-5, 5e-3, 1.1)
+    pre = PrefillParams(0.004, 128.0, 2e-5, 1.5e-3)
+    pred = LengthPredictor(mode="oracle", bucketing=Bucketing.equal_width(100, 4096))
+    cfgs = {"both": ScorpioConfig(), "r_only": ScorpioConfig(admission_min="r_only"),
+            "ttft_only": ScorpioConfig(tpot_guard=False), "tpot_only": ScorpioConfig(ttft_guard=False),
+            "neither": ScorpioConfig(False, False)}
+    blobs, meta = {}, []
+    for name, S, W, R, seed, fl in CASES:
+        a = config2_arrays(S, W, R, seed)
+        states = states_from_arrays(a, T)
+        adm, rej, bat, wait, vbs, mins, cred = [], [], [], [], [], [], []
+        for st in states:
+            p = plan_step(st, pred, itl, pre, cfgs[fl])
+            adm.append([e.request.id for e in p.admitted])
+            rej.append([w.request.id * 2 + (s.value == "rejected_admission") for w, s in p.rejected])
+            bat.append([e.request.id for e in p.decode_batch])
+            wait.append([w.request.id for w in st.waiting])
+            vbs.append(p.vbs)
+            mins.append(float("nan") if p.min_slo is None else p.min_slo)
+            E = int(a["credit_exp"][0])
+            from fractions import Fraction
+            for e in st.running[: len(st.running) - len(p.admitted)]:
+                n = e.credit * Fraction(e.request.tpot_slo) / Fraction(2) ** E
+                assert n.denominator == 1
+                cred.append(int(n))
+        k = f"{name}_"
+        for key, lists in (("adm", adm), ("rej", rej), ("bat", bat), ("wait", wait)):
+            blobs[k + key] = np.array([x for l in lists for x in l], np.int64)
+            blobs[k + key + "_n"] = np.array([len(l) for l in lists], np.int64)
+        blobs[k + "vbs"] = np.array(vbs)
+        blobs[k + "min_slo"] = np.array(mins)
+        blobs[k + "credit"] = np.array(cred, np.uint64)
+        meta.append(dict(name=name, segments=S, w=W, r=R, seed=seed, flags=fl))
+        print(name, "admitted", sum(map(len, adm)), "rejected", sum(map(len, rej)),
+              "batch", sum(map(len, bat)))
+    np.savez_compressed(os.path.join(HERE, "plan.npz"), **blobs)
+    json.dump(meta, open(os.path.join(HERE, "plan.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
