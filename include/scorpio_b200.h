@@ -196,6 +196,8 @@ int sl_run_batch_launches(void);
 #define SL_PLAN_REJECTED_ADMISSION 2
 #define SL_PLAN_ADMITTED 3
 #define SL_PLAN_GUARD_ONLY 64 /* flag: ttft_guard alone (no admission, sched_scorpio.py:183) */
+#define SL_PLAN_FCFS_WALK 128 /* flag: TTFT walk over the unsorted FCFS queue
+                                 (early_reject, sched_baselines.py:89-106) */
 
 typedef struct {
   int32_t n_segments;

@@ -111,6 +111,7 @@ class SlPlanOut(C.Structure):
 
 PLAN_WAITING, PLAN_REJECTED_TTFT, PLAN_REJECTED_ADMISSION, PLAN_ADMITTED = 0, 1, 2, 3
 PLAN_GUARD_ONLY = 64
+PLAN_FCFS_WALK = 128
 
 
 class SlPredictor(C.Structure):

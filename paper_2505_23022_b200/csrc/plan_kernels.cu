@@ -186,6 +186,7 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
   const bool r_only = cfg.flags & SL_FLAG_R_ONLY;
   const bool guard_only = cfg.flags & SL_PLAN_GUARD_ONLY;
+  const bool walk = ttft_guard || (cfg.flags & SL_PLAN_FCFS_WALK);
   const int64_t wb = st.w_begin[seg], rb = st.r_begin[seg];
   const int W = (int)(st.w_begin[seg + 1] - wb);
   const int R = (int)(st.r_begin[seg + 1] - rb);
@@ -211,7 +212,7 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
         tt = st.w_ttft[idx];
       }
       unsigned rejm = 0;
-      if (ttft_guard) {
+      if (walk) {
         int start = 0;
         while (start < cnt) {
           double run = prefix, mine = 0.0;
