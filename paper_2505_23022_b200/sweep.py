@@ -58,12 +58,11 @@ class SweepGrid:
 
 
 def shard_cells(n_cells: int, n_scales: int, rank: int, world: int) -> np.ndarray:
-    """Global cell ids owned by `rank`: cells are ordered rate-major, and taking
-    every world-th cell of the scale-major interleave gives every rank the same
-    rate mix."""
-    n_rates = n_cells // n_scales
-    ids = np.arange(n_cells).reshape(n_rates, n_scales).T.reshape(-1)  # scale-major walk
-    return np.sort(ids[rank::world])
+    """Global cell ids owned by `rank`: cells are ordered rate-major; rank r takes
+    the SLO scales s with s % world == r at EVERY rate, so every rank gets the
+    same rate mix and hence the same expected work."""
+    ids = np.arange(n_cells)
+    return ids[(ids % n_scales) % world == rank]
 
 
 def build_local(grid: SweepGrid, rank: int = 0, world: int = 1, outcomes: bool = False,
