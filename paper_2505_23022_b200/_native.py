@@ -16,7 +16,7 @@ import numpy as np
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB_DIR = os.path.join(PKG, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libscorpio_b200.so")
+LIB_PATH = os.environ.get("SL_LIB_PATH") or os.path.join(LIB_DIR, "libscorpio_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
 CSRC = os.path.join(PKG, "csrc")
 SOURCES = ("sim_kernel.cu", "plan_kernels.cu", "predict_kernel.cu")
