@@ -156,7 +156,7 @@ def run_reference_arm(args) -> None:
     steps_rs, steps_dt = [], []
     desc = ""
     for it in range(args.warmup + args.steps):
-        rs, dt, n, desc = cpu_reference(grid, args.cpu_sample, args.cpu_budget, threads)
+        rs, dt, n, desc = cpu_reference(grid, args.cpu_sample, args.ref_budget, threads)
         if it >= args.warmup:
             steps_rs.append(rs)
             steps_dt.append(dt)
@@ -171,6 +171,52 @@ def run_reference_arm(args) -> None:
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
+    """Config 2: one batched plan_step over 64k active requests:
+    1,024 segments x (32 waiting + 32 running), plus the 1 x (32,768 + 32,768)
+    stress segment.  The three kernels (LDF sort, guard+admission scan, credit
+    select) are timed separately with CUDA events, L2 flushed in between.
+    Algorithmic bytes per item: sort 16 B per waiting item,
+    scan 52 B per waiting + 8 B per running item, select 48 B per running item."""
+    import torch
+
+    from paper_2505_23022_b200.plan import PlanBatch
+    from paper_2505_23022_b200.snapshot import config2_arrays, plan_arrays
+
+    itl, pre = (1e-6, 1e-3, 1e-5, 5e-3, 1.1), (0.004, 128.0, 2e-5, 1.5e-3)
+    l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    out = {}
+    for name, (S, W, R) in (("primary_1024x(32+32)", (1024, 32, 32)),
+                            ("stress_1x(32768+32768)", (1, 32768, 32768))):
+        pb = PlanBatch(arrays=plan_arrays(config2_arrays(S, W, R, seed=11)), device=dev)
+        Wt, Rt = S * W, S * R
+        phases = {"sort": lambda: pb.sort(), "scan": lambda: pb.guard_admit(3, itl, pre),
+                  "select": lambda: pb.select(3, True)}
+        times = {k: [] for k in phases}
+        for it in range(reps + 2):
+            for k, fn in phases.items():
+                l2.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if it >= 2:
+                    times[k].append(e0.elapsed_time(e1) / 1e3)
+        bytes_ = {"sort": 16 * Wt, "scan": 52 * Wt + 8 * Rt, "select": 48 * Rt}
+        rows = {}
+        for k in phases:
+            t = float(np.mean(times[k]))
+            rows[k] = {"us": 1e6 * t, "achieved_gbs": bytes_[k] / t / 1e9,
+                       "frac": bytes_[k] / t / 1e9 / peak}
+        total = sum(float(np.mean(v)) for v in times.values())
+        out[name] = {"request_steps": Wt + Rt, "us_per_step": 1e6 * total,
+                     "request_steps_per_s": (Wt + Rt) / total, "kernels": rows}
+    return out
 
 
 def run_ours(args) -> None:
@@ -307,6 +353,8 @@ def run_ours(args) -> None:
             "gpu_launches": args.steps * N.lib().sl_run_batch_launches(),
             "clocks": clk.summary(),
         }
+        if not args.no_plan and world == 1:
+            line["config2_plan_step"] = plan_microbench(dev, peak)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -323,8 +371,12 @@ def main() -> None:
     ap.add_argument("--scales", type=int, default=64, help="SLO scales per GPU")
     ap.add_argument("--n-requests", type=int, default=10_000)
     ap.add_argument("--cpu-sample", type=int, default=64)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0,
+                    help="seconds of CPU work for the cpu_baseline sample")
+    ap.add_argument("--ref-budget", type=float, default=6.0,
+                    help="seconds of CPU work per --impl reference step")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-plan", action="store_true", help="skip the config-2 plan microbench")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -57,15 +57,21 @@ __device__ __forceinline__ void put_slot(Slot<WIDE> (&sl)[kSlots], int pos, cons
   for (int k = 0; k < kSlots; ++k) sel_slot<WIDE>(sl[k], mine && k_at == k, e);
 }
 
+// Neumaier sum of 1/slo over the running set in order; the serial chain reads
+// its operands from a per-warp smem broadcast buffer `bc` (32 doubles).
 template <bool WIDE>
-__device__ __forceinline__ double running_inv_sum(const Slot<WIDE> (&sl)[kSlots], int R) {
+__device__ __forceinline__ double running_inv_sum(const Slot<WIDE> (&sl)[kSlots], int R, int lane,
+                                                  double* bc) {
   PySum ps;
   ps_init(ps);
 #pragma unroll
   for (int k = 0; k < kSlots; ++k) {
-    int cnt = min(32, R - 32 * k);
-    double x = sl[k].inv;
-    for (int t = 0; t < cnt; ++t) ps_add(ps, bcast(x, t));
+    const int cnt = min(32, R - 32 * k);
+    if (cnt <= 0) break;
+    bc[lane] = sl[k].inv;
+    __syncwarp();
+    for (int t = 0; t < cnt; ++t) ps_add(ps, bc[t]);
+    __syncwarp();
   }
   return ps_result(ps);
 }
@@ -80,11 +86,48 @@ __device__ __forceinline__ cred_t<WIDE> running_min(const Slot<WIDE> (&sl)[kSlot
   return warp_min_cred<WIDE>(m);
 }
 
-// TTFT prefix walk over wl[0, W) in list order, speculative-parallel
-// (ttft_guard sched_scorpio.py:196-205; early_reject sched_baselines.py:95-103).
-__device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W, int& nrej,
-                          double now, int64_t step, Acc& acc, int lane, int64_t lg_rej,
-                          int64_t cap_rej) {
+// TTFT prefix walk over wl[0, W) in list order (ttft_guard sched_scorpio.py:196-205;
+// early_reject sched_baselines.py:95-103).
+//  1. Certified pass: an upper bound U_j of the sequential prefix (warp scan in
+//     any order, inflated by (1 + 2^-30), which dominates the rounding error
+//     of any summation order for W < 2^20) and monotonicity of IEEE addition
+//     give est_j <= fl(fl(e_j + U_j) + pf_j); if that bound is <= ttft_j for
+//     every item, no item is rejected and the queue is unchanged -- exactly.
+//  2. Otherwise the exact walk, speculative-parallel: the sequential chain
+//     assuming all undecided items are kept, lane-parallel tests, ballot for the
+//     first rejection, restart after it.
+__device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W,
+                                          int& nrej, double now, int64_t step, Acc& acc, int lane,
+                                          int64_t lg_rej, int64_t cap_rej, double* bc) {
+  if (W < (1 << 20)) {
+    const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
+    double U = 0.0;
+    bool all_ok = true;
+    for (int c0 = 0; c0 < W && all_ok; c0 += 32) {
+      const int j = c0 + lane;
+      const bool valid = j < W;
+      double e = 0.0, pf = 0.0, tt = 0.0;
+      if (valid) {
+        const WRec& r = s.wr[s.wl[j]];
+        e = fsub_(now, r.arr);
+        pf = r.prefill;
+        tt = r.ttft;
+      }
+      double v = pf;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(SL_FULL, v, o);
+        if (lane >= o) v = fadd_(v, y);
+      }
+      double excl = __shfl_up_sync(SL_FULL, v, 1);
+      if (lane == 0) excl = 0.0;
+      const double Uj = fmul_(fadd_(U, excl), inflate);
+      all_ok = __all_sync(SL_FULL, !valid || fadd_(fadd_(e, Uj), pf) <= tt);
+      U = fmul_(fadd_(U, __shfl_sync(SL_FULL, v, 31)), inflate);
+    }
+    if (all_ok) return;
+  }
+  double* pre = bc + 32;
   double prefix = 0.0;
   int kept = 0;
   for (int c0 = 0; c0 < W; c0 += 32) {
@@ -100,35 +143,39 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
       pf = r.prefill;
       tt = r.ttft;
     }
+    bc[lane] = pf;
+    __syncwarp();
     unsigned rejm = 0;
     int start = 0;
     while (start < cnt) {
       // assume every undecided item is kept: exact sequential prefix chain
-      double run = prefix, mine = 0.0;
+      double run = prefix;
       for (int t = start; t < cnt; ++t) {
-        double x = bcast(pf, t);
-        if (lane == t) mine = run;
-        run = fadd_(run, x);
+        if (lane == 0) pre[t] = run;
+        run = fadd_(run, bc[t]);
       }
-      bool rj = lane >= start && lane < cnt && fadd_(fadd_(e, mine), pf) > tt;
-      unsigned m = __ballot_sync(SL_FULL, rj);
+      __syncwarp();
+      const double mine = pre[lane];
+      const bool rj = lane >= start && lane < cnt && fadd_(fadd_(e, mine), pf) > tt;
+      const unsigned m = __ballot_sync(SL_FULL, rj);
       if (m == 0) {
         prefix = run;
         break;
       }
-      int r = __ffs(m) - 1;  // first rejection; earlier items saw the true prefix
+      const int r = __ffs(m) - 1;  // first rejection; earlier items saw the true prefix
       rejm |= 1u << r;
-      prefix = bcast(mine, r);  // a rejected item leaves the prefix unchanged
+      prefix = pre[r];  // a rejected item leaves the prefix unchanged
       start = r + 1;
+      __syncwarp();
     }
-    bool r_ = valid && ((rejm >> lane) & 1u);
-    bool keep = valid && !r_;
-    unsigned km = __ballot_sync(SL_FULL, keep);
+    const bool r_ = valid && ((rejm >> lane) & 1u);
+    const bool keep = valid && !r_;
+    const unsigned km = __ballot_sync(SL_FULL, keep);
     __syncwarp();
     if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
     if (r_) {
-      int pos = nrej + __popc(rejm & lanemask_lt());
-      int64_t rid = s.id[idx];
+      const int pos = nrej + __popc(rejm & lanemask_lt());
+      const int64_t rid = s.id[idx];
       acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u);
       acc.rej_ttft++;
       if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_TTFT;
@@ -422,6 +469,13 @@ __device__ __forceinline__ void quiet_steps(const Sim& s, const KArgs& a, bool h
                                             Acc& acc, int lane, Slot<WIDE>* scr) {
   const sl_cost& C = s.cost;
   const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
+  // Digest items of the step end times are deferred: lane (step % 32) keeps the
+  // end of its step and the 32 items are hashed together (one SIMT pass per 32
+  // steps instead of one lane-0 pass per step).
+  int64_t base = step;      // first step of the current 32-step window
+  uint64_t end_bits = 0;    // this lane's pending end time (step base + lane)
+  bool have_end = false;
+  uint64_t key2 = digest_key((uint64_t)step, 2);
   while (R > 0 && R <= 32 && next_t > now && now < horizon) {
     ++n_plans;
     req_steps += R;
@@ -432,13 +486,9 @@ __device__ __forceinline__ void quiet_steps(const Sim& s, const KArgs& a, bool h
     if (live) sl[0].N = b ? N - sl[0].S : N;
     const unsigned bm = __ballot_sync(SL_FULL, b);
     const int nb = __popc(bm);
-    // sum of current_len over the batch: butterfly over the live lanes only
-    unsigned v = b ? (unsigned)sl[0].cur_len : 0u;
-    for (int off = 1; off < R; off <<= 1) v += __shfl_xor_sync(SL_FULL, v, off);
-    const unsigned blen = __shfl_sync(SL_FULL, v, 0);
+    const unsigned blen = __reduce_add_sync(SL_FULL, b ? (unsigned)sl[0].cur_len : 0u);
     if (b) {
-      acc.dig += digest_item_k(digest_key((uint64_t)step, 2), __popc(bm & lanemask_lt()),
-                               (uint64_t)sl[0].id);
+      acc.dig += digest_item_k(key2, __popc(bm & lanemask_lt()), (uint64_t)sl[0].id);
       sl[0].cur_len += 1;
       sl[0].rem -= 1;
     }
@@ -449,12 +499,22 @@ __device__ __forceinline__ void quiet_steps(const Sim& s, const KArgs& a, bool h
     else
       L = fdiv_((double)blen, (double)nb);
     const double end = fadd_(now, itl(C, nb, L));
-    if (lane == 0) acc.dig += digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
+    if (lane == (int)(step - base)) {
+      end_bits = (uint64_t)__double_as_longlong(end);
+      have_end = true;
+    }
     if (__any_sync(SL_FULL, live && sl[0].rem <= 0))
       retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
     now = end;
     ++step;
+    key2 += kDigStep;
+    if (step - base == 32) {
+      if (have_end) acc.dig += digest_item((uint64_t)(base + lane), 3, 0, end_bits);
+      have_end = false;
+      base = step;
+    }
   }
+  if (have_end) acc.dig += digest_item((uint64_t)(base + lane), 3, 0, end_bits);
 }
 
 template <bool WIDE>
@@ -535,11 +595,13 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     bool fits = true;
     if (W > 0) {
       if (scorpio) {
-        if (ttft_guard) spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej);
+        if (ttft_guard)
+          spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
+                    reinterpret_cast<double*>(scr));
         if (tpot_guard) {
           if (W > 0) {
             if (!g.inv_valid) {
-              g.inv = running_inv_sum<WIDE>(sl, R);
+              g.inv = running_inv_sum<WIDE>(sl, R, lane, reinterpret_cast<double*>(scr));
               g.inv_valid = true;
             }
             fits = spec_admit<WIDE>(s, a, has_out, W, R, sl, g, nadm, nrej, P, r_only, step, acc,
@@ -551,7 +613,8 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
         }
       } else {
         if (s.policy == SL_POLICY_EARLY_REJECT)
-          spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej);
+          spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
+                    reinterpret_cast<double*>(scr));
         int room = s.cap - R;
         int take = room > 0 ? min(room, W) : 0;
         if (take > 0)
