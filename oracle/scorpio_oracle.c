@@ -377,6 +377,13 @@ uint64_t orc_digest_item(uint64_t step, uint32_t tag, uint32_t pos, uint64_t val
   return y ^ (y >> 32);
 }
 
+/* batch id hash: low 32 bits of mix(id); the batch of a work step is the one
+ * item digest_item(step, 2, n_batch, sum of batch_hid mod 2^32). */
+static uint32_t orc_batch_hid(uint64_t id) {
+  uint64_t y = id * 0xD6E8FEB86659FD93ULL;
+  return (uint32_t)(y ^ (y >> 32));
+}
+
 static uint64_t dbits(double x) {
   uint64_t u;
   memcpy(&u, &x, 8);
@@ -546,9 +553,12 @@ int orc_run(const orc_trace* tr, const orc_sim_params* p, orc_outcomes* out, orc
       digest += orc_digest_item((uint64_t)step_idx, 1, (uint32_t)r,
                                 (uint64_t)s.id[pl.rej_idx[r]] * 2u +
                                     (pl.rej_reason[r] == ORC_STATUS_REJECTED_ADMISSION));
-    for (int64_t b = 0; b < pl.n_batch; b++)
-      digest += orc_digest_item((uint64_t)step_idx, 2, (uint32_t)b,
-                                (uint64_t)s.id[s.running[pl.batch[b]].idx]);
+    {
+      uint32_t bh = 0; /* the batch: one item over the sum of batch_hid (mod 2^32) */
+      for (int64_t b = 0; b < pl.n_batch; b++)
+        bh += orc_batch_hid((uint64_t)s.id[s.running[pl.batch[b]].idx]);
+      digest += orc_digest_item((uint64_t)step_idx, 2, (uint32_t)pl.n_batch, bh);
+    }
     digest += orc_digest_item((uint64_t)step_idx, 3, 0, dbits(end));
 
     if (log && log->step_cap > 0) {

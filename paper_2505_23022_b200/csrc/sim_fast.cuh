@@ -22,6 +22,44 @@ namespace sl {
 
 constexpr int kSlots = 2;
 constexpr int kRunCap = 32 * kSlots;
+#ifndef SL_QUIET_MODE
+#define SL_QUIET_MODE 0  // 0: serial quiet steps (default: best sweep throughput); 1: block steps
+#endif
+#ifndef SL_BLOCK_RMAX
+#define SL_BLOCK_RMAX 64
+#endif
+#ifndef SL_BLOCK_WMAX
+#define SL_BLOCK_WMAX 32
+#endif
+#ifndef SL_BLOCKED_MIN
+#define SL_BLOCKED_MIN 8  // min. block length bound for a blocked (waiting > 0) block
+#endif
+
+// Optional per-phase cycle accounting (profiling builds only: -DSL_PHASE_PROF,
+// read back with sl_phase_prof_read).  Slots 0-7: cycles per phase, 8-13: counts.
+#ifdef SL_PHASE_PROF
+constexpr int kProfSims = 1 << 16;
+constexpr int kProfSlots = 14;
+__device__ unsigned long long sl_prof_cycles[kProfSims][kProfSlots];
+#define SL_PROF_DECL              \
+  unsigned long long prof_acc[kProfSlots] = {0}; \
+  long long prof_t = clock64();
+#define SL_PROF_MARK(k)                 \
+  {                                     \
+    const long long t_ = clock64();     \
+    prof_acc[k] += (unsigned long long)(t_ - prof_t); \
+    prof_t = t_;                        \
+  }
+#define SL_PROF_COUNT(k, v) prof_acc[k] += (v);
+#define SL_PROF_WRITE(si)                                                  \
+  if (lane == 0 && (si) < kProfSims)                                       \
+    for (int k_ = 0; k_ < kProfSlots; ++k_) sl_prof_cycles[si][k_] = prof_acc[k_];
+#else
+#define SL_PROF_DECL
+#define SL_PROF_MARK(k)
+#define SL_PROF_COUNT(k, v)
+#define SL_PROF_WRITE(si)
+#endif
 
 template <bool WIDE>
 struct Slot {
@@ -186,6 +224,15 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     nrej += __popc(rejm);
   }
   W = kept;
+}
+
+// Position of the n-th (1-based) set bit of x; requires 1 <= n <= popc(x).
+__device__ __forceinline__ unsigned nth_set_bit(unsigned x, int n) {
+  unsigned lo = 0;  // invariant: popc(x & bits [0, lo)) < n
+#pragma unroll
+  for (unsigned w = 16; w; w >>= 1)
+    if (__popc(x & ((1u << (lo + w)) - 1u)) < n) lo += w;
+  return lo;
 }
 
 // Cached running-set aggregates (sched_scorpio.py:117-124), warp-uniform.
@@ -456,30 +503,26 @@ __device__ __forceinline__ void retire(const Sim& s, const KArgs& a, bool has_ou
   }
 }
 
-// Quiet steps: nothing waiting, no arrival due, <= 32 running, credit
-// batching, no decision log.  Exactly the general step restricted to that
-// case (no admission, so prefill_s is the empty sum 0 and now + 0 == now,
-// and the strictest entry always batches, so the step has work); kept as a
-// tight loop because these steps are the critical path of a sweep.
+// Serial quiet steps (nothing waiting, <= 32 running, credit batching, no
+// log): the general step restricted to that case, one step per iteration.
+// The digest items of the steps are deferred and hashed lane-parallel, 32
+// steps per pass (lane j keeps step base+j).
 template <bool WIDE>
-__device__ __forceinline__ void quiet_steps(const Sim& s, const KArgs& a, bool has_out,
-                                            Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
-                                            double& now, int64_t& step, int64_t& n_plans,
-                                            int64_t& req_steps, double next_t, bool has_h,
-                                            Acc& acc, int lane, Slot<WIDE>* scr) {
+__device__ __forceinline__ void quiet_serial(const Sim& s, const KArgs& a, bool has_out,
+                                             Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
+                                             double& now, int64_t& step, int64_t& n_plans,
+                                             int64_t& req_steps, double next_t, bool has_h,
+                                             Acc& acc, int lane, Slot<WIDE>* scr) {
   const sl_cost& C = s.cost;
   const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
-  // Digest items of the step end times are deferred: lane (step % 32) keeps the
-  // end of its step and the 32 items are hashed together (one SIMT pass per 32
-  // steps instead of one lane-0 pass per step).
-  int64_t base = step;      // first step of the current 32-step window
-  uint64_t end_bits = 0;    // this lane's pending end time (step base + lane)
-  bool have_end = false;
-  uint64_t key2 = digest_key((uint64_t)step, 2);
+  int64_t base = step;
+  uint64_t end_bits = 0;
+  uint32_t d_nb = 0, d_bh = 0;
+  bool have = false;
+  uint32_t hh = batch_hid((uint64_t)sl[0].id);
   while (R > 0 && R <= 32 && next_t > now && now < horizon) {
     ++n_plans;
     req_steps += R;
-    // select_batch (sched_scorpio.py:171-179), fixed point
     const bool live = lane < R;
     const cred_t<WIDE> N = sl[0].N + g.Smin;
     const bool b = live && N >= sl[0].S;
@@ -487,8 +530,8 @@ __device__ __forceinline__ void quiet_steps(const Sim& s, const KArgs& a, bool h
     const unsigned bm = __ballot_sync(SL_FULL, b);
     const int nb = __popc(bm);
     const unsigned blen = __reduce_add_sync(SL_FULL, b ? (unsigned)sl[0].cur_len : 0u);
+    const unsigned bh = __reduce_add_sync(SL_FULL, b ? hh : 0u);
     if (b) {
-      acc.dig += digest_item_k(key2, __popc(bm & lanemask_lt()), (uint64_t)sl[0].id);
       sl[0].cur_len += 1;
       sl[0].rem -= 1;
     }
@@ -501,20 +544,254 @@ __device__ __forceinline__ void quiet_steps(const Sim& s, const KArgs& a, bool h
     const double end = fadd_(now, itl(C, nb, L));
     if (lane == (int)(step - base)) {
       end_bits = (uint64_t)__double_as_longlong(end);
-      have_end = true;
+      d_nb = nb;
+      d_bh = bh;
+      have = true;
     }
-    if (__any_sync(SL_FULL, live && sl[0].rem <= 0))
+    if (__any_sync(SL_FULL, live && sl[0].rem <= 0)) {
       retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
+      hh = batch_hid((uint64_t)sl[0].id);
+    }
     now = end;
     ++step;
-    key2 += kDigStep;
     if (step - base == 32) {
-      if (have_end) acc.dig += digest_item((uint64_t)(base + lane), 3, 0, end_bits);
-      have_end = false;
+      if (have)
+        acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
+                   digest_item((uint64_t)(base + lane), 3, 0, end_bits);
+      have = false;
       base = step;
     }
   }
-  if (have_end) acc.dig += digest_item((uint64_t)(base + lane), 3, 0, end_bits);
+  if (have)
+    acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
+               digest_item((uint64_t)(base + lane), 3, 0, end_bits);
+}
+
+// Block steps: runs of consecutive scheduler steps in which the running set
+// does not change membership and no waiting request is admitted or rejected.
+// Two kinds qualify (credit batching, no decision log, <= 64 running):
+//  * quiet steps -- nothing waiting (~64% of the steps of a config-3 sweep);
+//  * blocked steps -- 1..32 waiting requests, every one feasible alone
+//    (solo_ok) and failing the admission test against the current running
+//    aggregates (_admission_math, sched_scorpio.py:83-114).  With membership
+//    fixed only `lens` changes, and it only grows, so the estimate (monotone
+//    in L for non-negative alpha/gamma/epsilon) keeps failing: the scan
+//    (sched_scorpio.py:234-294) admits and rejects nothing.  The TTFT walk
+//    (:196-205) is monotone in `now`, so the first step at which it would
+//    reject an item is found by bisection over the block's clock; the block
+//    ends before it.  (~22% of the steps.)
+// In both, a step's duration depends only on integer state (the empty
+// prefill sum is 0 and now + 0 == now; the strictest entry always batches):
+//  A. lane e runs its entries' credit recurrences (select_batch,
+//     sched_scorpio.py:171-179) for up to 32 steps: bit j of `bits` = entry
+//     batched at step j; the first retirement (the rem-th set bit) caps the block;
+//  B. per step j: batch size, the sum of current lengths and the batch id hash
+//     (ballot + redux), delivered to lane j;
+//  C. lane j evaluates its step's itl() (simengine.py:233-238) -- all 32 in
+//     parallel -- and only the clock now_{j+1} = now_j + d_j, which IEEE
+//     rounding makes order dependent, stays a serial chain (one DADD per
+//     step); the block ends before the first step whose start time sees an
+//     arrival (or the horizon) or at which the walk would reject;
+//  D. the K executed steps are committed: credits in closed form (exact mod
+//     2^w, the true value lies in [0, S)), digest items (lane j: step j),
+//     retirement.
+// Returns true when the next step must be a general step at the same `now`
+// (a waiting request would be admitted or rejected); false when the loop
+// ended on an arrival, the horizon, or the running-set size.
+template <bool WIDE>
+__device__ __forceinline__ bool block_steps(const Sim& s, const KArgs& a, bool has_out,
+                                            Slot<WIDE> (&sl)[kSlots], int& R, const int W,
+                                            Agg<WIDE>& g, double& now, int64_t& step,
+                                            int64_t& n_plans, int64_t& req_steps, double next_t,
+                                            bool has_h, bool walk, bool r_only, Acc& acc,
+                                            int lane, Slot<WIDE>* scr) {
+  const sl_cost& C = s.cost;
+  const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
+  double* bc = reinterpret_cast<double*>(scr);
+  double* dur = bc;        // [32] step durations
+  double* clk = bc + 32;   // [33] step start times, clk[jmax] = end of the block
+  // waiting requests (lane i = queue position i), fixed for the whole call
+  const bool wv = lane < W;
+  double w_arr = 0.0, w_pf = 0.0, w_tt = 0.0, w_pre = 0.0, w_tp = 0.0, w_ic = 0.0;
+  int32_t w_ln = 0, w_ps = 0;
+  if (W > 0 && !(C.alpha >= 0.0 && C.gamma >= 0.0 && C.epsilon >= 0.0)) return true;
+  bool wloaded = false;
+  while (R > 0 && R <= 64 && next_t > now && now < horizon) {
+    const bool two = R > 32;
+    const bool live0 = lane < R, live1 = 32 + lane < R;
+    // Block length cap (any cap is exact; it only sizes the work): every step
+    // lasts at least itl(1, min current length) when the coefficients are
+    // non-negative (itl is then monotone in B and L), so at most
+    // (stop - now) / dmin + 1 steps start before the next arrival / horizon.
+    int jcap = 32;
+    if (C.alpha >= 0.0 && C.beta >= 0.0 && C.gamma >= 0.0 && C.delta > 0.0) {
+      unsigned ml = live0 ? (unsigned)sl[0].cur_len : ~0u;
+      if (live1) ml = min(ml, (unsigned)sl[1].cur_len);
+      const unsigned mlen = __reduce_min_sync(SL_FULL, ml);
+      const double dmin = itl(C, 1, (double)mlen);
+      const double span = fsub_(fmin(next_t, horizon), now);
+      if (span < 31.0 * dmin) jcap = 1 + (int)(span / dmin);
+    }
+    if (W > 0 && jcap < SL_BLOCKED_MIN) return true;  // too short to pay for itself
+    if (W > 0 && !wloaded) {  // load the waiting requests once per call
+      wloaded = true;
+      if (wv) {
+        const WRec& w = s.wr[s.wl[lane]];
+        w_arr = w.arr;
+        w_pf = w.prefill;
+        w_tt = w.ttft;
+        w_tp = w.tpot;
+        w_ic = w.inv;
+        w_ln = w.prompt;
+        w_ps = w.pred_solo;
+      }
+      if (!__all_sync(SL_FULL, !wv || (w_ps & (int32_t)0x80000000) != 0)) return true;
+      if (walk) {  // exact sequential prefix of the walk (nothing is rejected in a block)
+        dur[lane] = w_pf;
+        __syncwarp();
+        double t = 0.0;
+        for (int i = 0; i < W; ++i) {
+          if (lane == i) w_pre = t;
+          t = fadd_(t, dur[i]);
+        }
+        __syncwarp();
+      }
+    }
+    if (W > 0) {  // every waiting request fails the admission test at the current state
+      if (!g.inv_valid) {
+        g.inv = running_inv_sum<WIDE>(sl, R, lane, bc);
+        g.inv_valid = true;
+      }
+      const double mind = g.min_d;
+      const bool lt = w_tp < mind;
+      const double minp = lt ? w_tp : mind;
+      const double V = fmul_(minp, fadd_(g.inv, w_ic));
+      const double L = fdiv_((double)(g.lens + w_ln), (double)(R + 1));
+      const double est = tpot_estimate(C, V, L, w_ps & 0x7fffffff);
+      const double thr = r_only ? mind : minp;
+      if (__any_sync(SL_FULL, wv && est <= thr)) return true;
+    }
+    // A. credit recurrences for jcap steps (all 32 when jcap == 32)
+    const cred_t<WIDE> M = g.Smin;
+    unsigned bits[kSlots];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
+      bits[k] = 0u;
+      if (k == 1 && !two) break;
+      const cred_t<WIDE> S = sl[k].S;
+      cred_t<WIDE> N = sl[k].N;
+      if (jcap == 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          N += M;
+          const bool b = N >= S;
+          N = b ? N - S : N;
+          bits[k] |= (unsigned)b << j;
+        }
+      } else {
+        for (int j = 0; j < jcap; ++j) {
+          N += M;
+          const bool b = N >= S;
+          N = b ? N - S : N;
+          bits[k] |= (unsigned)b << j;
+        }
+      }
+    }
+    bits[0] = live0 ? bits[0] : 0u;
+    if (kSlots > 1) bits[1] = live1 ? bits[1] : 0u;
+    unsigned rj = (live0 && sl[0].rem <= __popc(bits[0])) ? nth_set_bit(bits[0], sl[0].rem) : 32u;
+    if (live1 && sl[1].rem <= __popc(bits[1])) rj = min(rj, nth_set_bit(bits[1], sl[1].rem));
+    const int jmax = min(jcap, (int)__reduce_min_sync(SL_FULL, rj) + 1);
+    // B. batch size, length sum and id-hash sum of step j -> lane j
+    int my_nb = 0;
+    unsigned my_blen = 0, my_bh = 0;
+    {
+      unsigned cl0 = live0 ? (unsigned)sl[0].cur_len : 0u;
+      unsigned cl1 = live1 ? (unsigned)sl[1].cur_len : 0u;
+      const unsigned h0 = batch_hid((uint64_t)sl[0].id);
+      const unsigned h1 = two ? batch_hid((uint64_t)sl[1].id) : 0u;
+      for (int j = 0; j < jmax; ++j) {
+        const bool b0 = (bits[0] >> j) & 1u;
+        const bool b1 = (bits[1] >> j) & 1u;
+        const int nb = (int)__reduce_add_sync(SL_FULL, (unsigned)b0 + (unsigned)b1);
+        const unsigned bl = __reduce_add_sync(SL_FULL, (b0 ? cl0 : 0u) + (b1 ? cl1 : 0u));
+        const unsigned bh = __reduce_add_sync(SL_FULL, (b0 ? h0 : 0u) + (b1 ? h1 : 0u));
+        cl0 += b0;
+        cl1 += b1;
+        if (lane == j) {
+          my_nb = nb;
+          my_blen = bl;
+          my_bh = bh;
+        }
+      }
+    }
+    // C. step durations in parallel; the clock chain serially
+    if (lane < jmax) dur[lane] = itl(C, my_nb, fdiv_((double)my_blen, (double)my_nb));
+    __syncwarp();
+    {
+      double t = now;
+      for (int j = 0; j < jmax; ++j) {
+        if (lane == 0) clk[j] = t;
+        t = fadd_(t, dur[j]);
+      }
+      if (lane == 0) clk[jmax] = t;
+    }
+    __syncwarp();
+    const double my_start = clk[lane];
+    const double my_end = clk[lane + 1];
+    // first step at which the walk would reject a waiting request (bisection;
+    // est is monotone in now)
+    int jw = 32;
+    if (W > 0 && walk) {
+      int lo = 0, hi = jmax;  // first j in [0, jmax) with est(clk[j]) > ttft, else jmax
+      if (wv) {
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (fadd_(fadd_(fsub_(clk[mid], w_arr), w_pre), w_pf) > w_tt)
+            hi = mid;
+          else
+            lo = mid + 1;
+        }
+      } else {
+        lo = jmax;
+      }
+      jw = (int)__reduce_min_sync(SL_FULL, (unsigned)lo);
+    }
+    __syncwarp();
+    const unsigned runm =
+        __ballot_sync(SL_FULL, lane < jmax && lane < jw && next_t > my_start && my_start < horizon);
+    const int K = (~runm == 0u) ? 32 : __ffs(~runm) - 1;
+    if (K == 0) return true;  // the walk rejects at this very step
+    // D. commit steps [0, K)
+    const unsigned km = K == 32 ? ~0u : ((1u << K) - 1u);
+    int csum = 0;
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
+      const bool live = k == 0 ? live0 : live1;
+      const int c = __popc(bits[k] & km);
+      if (live) {
+        sl[k].N = sl[k].N + (cred_t<WIDE>)K * M - (cred_t<WIDE>)c * sl[k].S;
+        sl[k].cur_len += c;
+        sl[k].rem -= c;
+      }
+      csum += c;
+    }
+    g.lens += __reduce_add_sync(SL_FULL, (unsigned)csum);
+    n_plans += K;
+    req_steps += (int64_t)K * (R + W);
+    if (lane < K)
+      acc.dig += digest_item((uint64_t)(step + lane), 2, (uint32_t)my_nb, my_bh) +
+                 digest_item((uint64_t)(step + lane), 3, 0, (uint64_t)__double_as_longlong(my_end));
+    const double end = __shfl_sync(SL_FULL, my_end, K - 1);
+    step += K;
+    __syncwarp();
+    if (__any_sync(SL_FULL, (live0 && sl[0].rem <= 0) || (live1 && sl[1].rem <= 0)))
+      retire<WIDE>(s, a, has_out, sl, R, g, end, step - 1, acc, lane, scr);
+    now = end;
+    // walk rejection due at the next step, no arrival pending: a general step follows
+    if (K == jw && next_t > now && now < horizon) return true;
+  }
+  return false;
 }
 
 template <bool WIDE>
@@ -566,16 +843,39 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
   int W = 0, R = 0;
   int64_t step = 0, n_plans = 0, n_idle = 0, req_steps = 0;
   int status = SL_SIM_OK;
+  SL_PROF_DECL
 
   for (;;) {
     if (next < n && next_t <= now)
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
+    SL_PROF_MARK(0)
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
+#if SL_QUIET_MODE == 0
     if (W == 0 && credit && !logging && R > 0 && R <= 32) {
-      quiet_steps<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t, has_h, acc,
-                        lane, scr);
+      SL_PROF_COUNT(9, 1)
+      SL_PROF_COUNT(10, -step)
+      quiet_serial<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t, has_h,
+                         acc, lane, scr);
+      SL_PROF_COUNT(10, step)
+      SL_PROF_MARK(1)
       continue;
     }
+    if (false) {
+#else
+    if (credit && !logging && R > 0 && R <= SL_BLOCK_RMAX && W <= SL_BLOCK_WMAX) {
+#endif
+      SL_PROF_COUNT(9, 1)
+      SL_PROF_COUNT(10, -step)
+      const bool general = block_steps<WIDE>(s, a, has_out, sl, R, W, g, now, step, n_plans,
+                                             req_steps, next_t, has_h, ttft_guard, r_only, acc,
+                                             lane, scr);
+      SL_PROF_COUNT(10, step)
+      SL_PROF_MARK(1)
+      if (!general) continue;
+    }
+    SL_PROF_COUNT(8, 1)
+    SL_PROF_COUNT(12, W == 0)
+    SL_PROF_COUNT(13, R > 32)
 
     ++n_plans;
     req_steps += W + R;
@@ -598,12 +898,14 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
         if (ttft_guard)
           spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
                     reinterpret_cast<double*>(scr));
+        SL_PROF_MARK(2)
         if (tpot_guard) {
           if (W > 0) {
             if (!g.inv_valid) {
               g.inv = running_inv_sum<WIDE>(sl, R, lane, reinterpret_cast<double*>(scr));
               g.inv_valid = true;
             }
+            SL_PROF_MARK(3)
             fits = spec_admit<WIDE>(s, a, has_out, W, R, sl, g, nadm, nrej, P, r_only, step, acc,
                                     lane, lg_adm, cap_adm, lg_rej, cap_rej);
           }
@@ -626,10 +928,11 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       status = SL_SIM_CAPACITY;
       break;
     }
+    SL_PROF_MARK(4)
 
     // ---- decode batch: credit phase (select_batch :161-180) or decode-all
     unsigned bm[kSlots];
-    unsigned blen = 0;
+    unsigned blen = 0, bhash = 0;
     int nb = 0;
     const bool decode = credit || !(prio && nadm > 0);
 #pragma unroll
@@ -647,9 +950,9 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       }
       bm[k] = __ballot_sync(SL_FULL, b);
       blen += __reduce_add_sync(SL_FULL, b ? (unsigned)sl[k].cur_len : 0u);
+      bhash += __reduce_add_sync(SL_FULL, b ? batch_hid((uint64_t)sl[k].id) : 0u);
       if (b) {
         int pos = nb + __popc(bm[k] & lanemask_lt());
-        acc.dig += digest_item((uint64_t)step, 2, (uint32_t)pos, (uint64_t)sl[k].id);
         if (lg_bat >= 0 && pos < cap_bat) a.log.batch_ids[lg_bat + pos] = sl[k].id;
         sl[k].cur_len += 1;  // token emit (simengine.py:243-245), after l_avg's input
         sl[k].rem -= 1;
@@ -657,6 +960,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       nb += __popc(bm[k]);
     }
     g.lens += nb;
+    SL_PROF_MARK(5)
 
     // ---- no work: idle skip (simengine.py:207-227)
     if (nadm == 0 && nb == 0) {
@@ -711,7 +1015,9 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     }
     const double end = fadd_(fadd_(now, prefill_s), decode_s);
     acc.dig += acc.dig_rej;
-    if (lane == 0) acc.dig += digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
+    if (lane == 0)
+      acc.dig += digest_item((uint64_t)step, 2, (uint32_t)nb, bhash) +
+                 digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
 
     // ---- decision log row (EventLog.steps)
     if (logging) {
@@ -771,10 +1077,14 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
 #pragma unroll
     for (int k = 0; k < kSlots; ++k)
       any_ret |= __any_sync(SL_FULL, 32 * k + lane < R && sl[k].rem <= 0);
+    SL_PROF_MARK(6)
     if (any_ret) retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
+    SL_PROF_COUNT(11, W > 0 && nadm == 0 && nrej == 0)
+    SL_PROF_MARK(7)
     now = end;
     ++step;
   }
+  SL_PROF_WRITE(si)
 
   write_result(a, si, acc, status | (log_over ? SL_SIM_LOG_OVERFLOW : 0), n, step, n_plans,
                n_idle, req_steps, now, has_h, s.horizon, lane);

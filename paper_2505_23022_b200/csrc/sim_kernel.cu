@@ -25,6 +25,7 @@
 #include "sl_device.cuh"
 #include "sim_common.cuh"
 #include "sim_fast.cuh"
+#include <stdlib.h>
 
 using namespace sl;
 
@@ -234,6 +235,7 @@ __device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_inde
     PySum P;
     ps_init(P);
     int64_t blen = 0;  // per-lane partial of sum(current_len) over the batch
+    uint32_t bhash = 0;  // per-lane partial of the batch id hash sum (digest tag 2)
     acc.dig_rej = 0;
     int64_t lg_adm = (logging && !log_over) ? lg_id0 + cur_adm : -1;
     int64_t lg_rej = (logging && !log_over) ? lg_id0 + cur_rej : -1;
@@ -420,7 +422,7 @@ __device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_inde
           r.cur_len += 1;  // token emit (simengine.py:243-245); l_avg already taken
           r.rem -= 1;
           int64_t rid = s.id[s.rl[j]];
-          acc.dig += digest_item((uint64_t)step, 2, (uint32_t)pos, (uint64_t)rid);
+          bhash += batch_hid((uint64_t)rid);
           if (lg_bat >= 0 && pos < cap_bat) a.log.batch_ids[lg_bat + pos] = rid;
         }
         nbatch += __popc(bm);
@@ -472,7 +474,10 @@ __device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_inde
     if (nbatch > 0) decode_s = itl(C, nbatch, fdiv_((double)bl, (double)nbatch));
     double end = fadd_(fadd_(now, prefill_s), decode_s);
     acc.dig += acc.dig_rej;
-    if (lane == 0) acc.dig += digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
+    bhash = __reduce_add_sync(SL_FULL, bhash);
+    if (lane == 0)
+      acc.dig += digest_item((uint64_t)step, 2, (uint32_t)nbatch, bhash) +
+                 digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
 
     // ---- decision log row
     if (logging) {
@@ -607,7 +612,10 @@ __global__ void __launch_bounds__(128) sl_sim_kernel(const __grid_constant__ KAr
 // Fast kernel: running set in registers (sim_fast.cuh); hands off sims that
 // outgrow it or are flagged general-only.
 constexpr int kFastWarps = 4;
-__global__ void __launch_bounds__(32 * kFastWarps) sl_sim_fast_kernel(
+#ifndef SL_FAST_MIN_BLOCKS
+#define SL_FAST_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(32 * kFastWarps, SL_FAST_MIN_BLOCKS) sl_sim_fast_kernel(
     const __grid_constant__ KArgs a) {
   __shared__ Slot<false> scratch[kFastWarps][kRunCap];
   const int lane = threadIdx.x & 31;
@@ -666,6 +674,15 @@ int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_
 }
 
 int sl_run_batch_launches(void) { return 2; }
+
+#ifdef SL_PHASE_PROF
+// Profiling builds only: per-sim phase cycles / counts of the fast kernel.
+int sl_phase_prof_read(uint64_t* out, int32_t n_sims) {
+  if (n_sims > kProfSims) n_sims = kProfSims;
+  return cudaMemcpyFromSymbol(out, sl_prof_cycles, sizeof(unsigned long long) * kProfSlots * n_sims) ==
+                 cudaSuccess ? n_sims : SL_ERR_CUDA;
+}
+#endif
 
 int sl_abi_layout(int64_t* out, int32_t n) {
   if (!out || n < 7) return SL_ERR_ARG;
@@ -726,6 +743,10 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
   auto grid_for = [&](const void* fn, int threads) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+    if (const char* e = getenv("SL_BLOCKS_PER_SM")) {  // experiments: cap residency
+      int cap = atoi(e);
+      if (cap > 0 && cap < per_sm) per_sm = cap;
+    }
     if (per_sm < 1) per_sm = 1;
     int64_t wpb = threads / 32;
     int64_t blocks = (n_sims + wpb - 1) / wpb;

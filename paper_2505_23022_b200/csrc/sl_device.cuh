@@ -165,7 +165,9 @@ __device__ __forceinline__ cred_t<WIDE> warp_min_cred(cred_t<WIDE> v) {
 
 // ---- work-step decision digest (oracle orc_digest_item).
 // item = mix(val ^ (step*K_STEP + tag*K_TAG + pos*K_POS)), mix(x) = (x*K_MIX) ^ ((x*K_MIX) >> 32);
-// the digest is the sum mod 2^64 of the items of all work steps.
+// the digest is the sum mod 2^64 of the items of all work steps: per admitted
+// id (tag 0), per rejection (tag 1), one per step for the batch (tag 2, see
+// batch_hid) and one per step for the end time (tag 3).
 constexpr uint64_t kDigStep = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t kDigTag = 0xC2B2AE3D27D4EB4FULL;
 constexpr uint64_t kDigPos = 0x165667B19E3779F9ULL;
@@ -180,6 +182,13 @@ __device__ __forceinline__ uint64_t digest_item_k(uint64_t key, uint32_t pos, ui
 __device__ __forceinline__ uint64_t digest_item(uint64_t step, uint32_t tag, uint32_t pos,
                                                 uint64_t val) {
   return digest_item_k(digest_key(step, tag), pos, val);
+}
+// Batch id hash: the low 32 bits of mix(id).  The batch of a work step enters
+// the digest as ONE item, digest_item(step, 2, n_batch, sum of batch_hid mod
+// 2^32) -- a warp reduction per step instead of a hash per (step, entry).
+__device__ __forceinline__ uint32_t batch_hid(uint64_t id) {
+  const uint64_t y = id * kDigMix;
+  return (uint32_t)(y ^ (y >> 32));
 }
 
 }  // namespace sl

@@ -44,8 +44,11 @@ def log_digest(log) -> int:
             h += digest_item(s_idx, 0, pos, rid)
         for pos, (rid, reason) in enumerate(rec.rejected):
             h += digest_item(s_idx, 1, pos, rid * 2 + (reason == "rejected_admission"))
-        for pos, rid in enumerate(rec.batch):
-            h += digest_item(s_idx, 2, pos, rid)
+        bh = 0  # the batch: one item over sum(batch_hid) mod 2^32
+        for rid in rec.batch:
+            y = ((rid & M64) * 0xD6E8FEB86659FD93) & M64
+            bh += (y ^ (y >> 32)) & 0xFFFFFFFF
+        h += digest_item(s_idx, 2, len(rec.batch), bh & 0xFFFFFFFF)
         h += digest_item(s_idx, 3, 0, dbits(rec.end_s))
     return h & M64
 

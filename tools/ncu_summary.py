@@ -17,7 +17,9 @@ def raw(rep):
     rows = list(csv.reader(out.splitlines()))
     h, u, v = rows[0], rows[1], rows[2]
     d = dict(zip(h, v))
-    res = {k: d.get(k) for k in KEYS}
+    units = dict(zip(h, u))
+    res = {k: (f"{d.get(k)} {units.get(k, '')}".strip() if d.get(k) is not None else None)
+           for k in KEYS}
     stalls = {k.split("issue_stalled_")[1].replace("_per_issue_active.ratio", ""): float(x)
               for k, x in d.items() if "average_warps_issue_stalled" in k and x not in ("", "n/a")}
     return res, stalls

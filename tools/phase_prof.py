@@ -1,0 +1,42 @@
+"""Per-phase cycle accounting of the fast sweep kernel (profiling build, -DSL_PHASE_PROF).
+
+usage: SL_LIB_PATH=paper_2505_23022_b200/lib/libvar_prof.so python tools/phase_prof.py [rates scales]
+Prints per-phase cycle totals over all sims and for the longest sim."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2505_23022_b200 import _native as N  # noqa: E402
+from paper_2505_23022_b200.sweep import SweepGrid, build_local  # noqa: E402
+
+nr = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+ns = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+grid = SweepGrid(rates=tuple(np.linspace(2.0, 32.0, nr)), scales=tuple(np.geomspace(0.5, 2.0, ns)))
+eng, owned, _ = build_local(grid, device=torch.device("cuda", 0))
+eng.launch()
+torch.cuda.synchronize()
+res = eng.results()
+lib = N.lib()
+lib.sl_phase_prof_read.argtypes = [C.c_void_p, C.c_int32]
+out = np.zeros((eng.n_sims, 14), np.uint64)
+assert lib.sl_phase_prof_read(out.ctypes.data, eng.n_sims) == eng.n_sims
+names = ["arrivals+top", "quiet", "walk", "inv_sum", "admit", "decode", "tail", "retire",
+         "gen_steps", "quiet_blocks", "quiet_steps", "gen_blocked", "gen_W0", "gen_R>32"]
+cyc = out[:, :8].astype(np.float64)
+tot = cyc.sum(axis=0)
+print("all sims: total cycles %.3e (%d sims); per-phase share:" % (tot.sum(), eng.n_sims))
+for k in range(8):
+    print(f"  {names[k]:14s} {100 * tot[k] / tot.sum():5.1f}%   {tot[k] / max(1, out[:, 8].sum()):8.1f} cyc/gen-step")
+cnt = out[:, 8:].sum(axis=0)
+print("counts:", dict(zip(names[8:], cnt.tolist())), "sim steps", int(res["n_steps"].sum()),
+      "request_steps", int(res["request_steps"].sum()))
+print("quiet: %.1f cyc/quiet-step, %.2f steps/block" % (tot[1] / max(1, cnt[2]), cnt[2] / max(1, cnt[1])))
+i = int(np.argmax(cyc.sum(axis=1)))
+print(f"longest sim {i}: {cyc[i].sum():.3e} cycles, steps {int(res['n_steps'][i])}")
+for k in range(8):
+    print(f"  {names[k]:14s} {100 * cyc[i, k] / cyc[i].sum():5.1f}%")
+print("  counts", out[i, 8:].tolist())
