@@ -233,7 +233,7 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
   const sl_cost& C = s.cost;
   while (next < s.n && next_t <= now) {
     int64_t i = next + lane;
-    double ai = (i < s.n) ? fdiv_(s.arrival[i], s.factor) : kInf;
+    double ai = (i < s.n) ? (s.factor == 1.0 ? s.arrival[i] : fdiv_(s.arrival[i], s.factor)) : kInf;
     bool c = ai <= now;
     unsigned m = __ballot_sync(SL_FULL, c);
     int k = __popc(m);  // arrivals are sorted: m is a lane prefix
@@ -263,7 +263,7 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
       W += k;
     }
     next += k;
-    next_t = next < s.n ? fdiv_(s.arrival[next], s.factor) : kInf;
+    next_t = next < s.n ? (s.factor == 1.0 ? s.arrival[next] : fdiv_(s.arrival[next], s.factor)) : kInf;
   }
 }
 

@@ -98,8 +98,8 @@ __device__ __forceinline__ void put_slot(Slot<WIDE> (&sl)[kSlots], int pos, cons
 // Neumaier sum of 1/slo over the running set in order; the serial chain reads
 // its operands from a per-warp smem broadcast buffer `bc` (32 doubles).
 template <bool WIDE>
-__device__ __forceinline__ double running_inv_sum(const Slot<WIDE> (&sl)[kSlots], int R, int lane,
-                                                  double* bc) {
+__device__ __forceinline__ PySum running_inv_sum(const Slot<WIDE> (&sl)[kSlots], int R, int lane,
+                                                 double* bc) {
   PySum ps;
   ps_init(ps);
 #pragma unroll
@@ -111,7 +111,7 @@ __device__ __forceinline__ double running_inv_sum(const Slot<WIDE> (&sl)[kSlots]
     for (int t = 0; t < cnt; ++t) ps_add(ps, bc[t]);
     __syncwarp();
   }
-  return ps_result(ps);
+  return ps;
 }
 
 template <bool WIDE>
@@ -124,6 +124,25 @@ __device__ __forceinline__ cred_t<WIDE> running_min(const Slot<WIDE> (&sl)[kSlot
   return warp_min_cred<WIDE>(m);
 }
 
+// Time up to which the walk provably rejects nothing: item j passed at `now`
+// with prefix bound U (est0 = fl(fl(fl(now - arr) + U) + pf) <= ttft); its est
+// at a later now1 (prefix <= U: prefixes only shrink until an insertion) stays
+// <= ttft while now1 - now < sigma - m, sigma = fl(ttft - est0) and
+// m = 2^-40 * 2 * (now + U + pf + sigma) >> the <= 8u relative rounding error
+// of the three-op chain evaluated at now and now1.
+__device__ __forceinline__ double walk_pass_until(double now, double U, double pf, double tt,
+                                                  double est0) {
+  const double sig = fsub_(tt, est0);
+  const double m = fmul_(1.8189894035458565e-12, fadd_(fadd_(fadd_(now, U), pf), sig));  // 2^-39 *
+  return fsub_(fadd_(now, sig), m);
+}
+
+__device__ __forceinline__ double warp_min_d(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(SL_FULL, v, o));
+  return v;
+}
+
 // TTFT prefix walk over wl[0, W) in list order (ttft_guard sched_scorpio.py:196-205;
 // early_reject sched_baselines.py:95-103).
 //  1. Certified pass: an upper bound U_j of the sequential prefix (warp scan in
@@ -134,12 +153,17 @@ __device__ __forceinline__ cred_t<WIDE> running_min(const Slot<WIDE> (&sl)[kSlot
 //  2. Otherwise the exact walk, speculative-parallel: the sequential chain
 //     assuming all undecided items are kept, lane-parallel tests, ballot for the
 //     first rejection, restart after it.
+// `until` receives the time before which the walk over the remaining queue
+// rejects nothing (walk_pass_until), valid until the next insertion.
 __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W,
                                           int& nrej, double now, int64_t step, Acc& acc, int lane,
-                                          int64_t lg_rej, int64_t cap_rej, double* bc) {
+                                          int64_t lg_rej, int64_t cap_rej, double* bc,
+                                          double& until) {
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   if (W < (1 << 20)) {
     const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
     double U = 0.0;
+    double tmin = kInf;
     bool all_ok = true;
     for (int c0 = 0; c0 < W && all_ok; c0 += 32) {
       const int j = c0 + lane;
@@ -160,13 +184,19 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
       double excl = __shfl_up_sync(SL_FULL, v, 1);
       if (lane == 0) excl = 0.0;
       const double Uj = fmul_(fadd_(U, excl), inflate);
-      all_ok = __all_sync(SL_FULL, !valid || fadd_(fadd_(e, Uj), pf) <= tt);
+      const double est0 = fadd_(fadd_(e, Uj), pf);
+      all_ok = __all_sync(SL_FULL, !valid || est0 <= tt);
+      if (valid) tmin = fmin(tmin, walk_pass_until(now, Uj, pf, tt, est0));
       U = fmul_(fadd_(U, __shfl_sync(SL_FULL, v, 31)), inflate);
     }
-    if (all_ok) return;
+    if (all_ok) {
+      until = warp_min_d(tmin);
+      return;
+    }
   }
   double* pre = bc + 32;
   double prefix = 0.0;
+  double tmin = kInf;
   int kept = 0;
   for (int c0 = 0; c0 < W; c0 += 32) {
     const int j = c0 + lane;
@@ -208,6 +238,10 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     }
     const bool r_ = valid && ((rejm >> lane) & 1u);
     const bool keep = valid && !r_;
+    if (keep) {
+      const double mine = pre[lane];
+      tmin = fmin(tmin, walk_pass_until(now, mine, pf, tt, fadd_(fadd_(e, mine), pf)));
+    }
     const unsigned km = __ballot_sync(SL_FULL, keep);
     __syncwarp();
     if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
@@ -224,6 +258,7 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     nrej += __popc(rejm);
   }
   W = kept;
+  until = warp_min_d(tmin);
 }
 
 // Position of the n-th (1-based) set bit of x; requires 1 <= n <= popc(x).
@@ -241,8 +276,8 @@ struct Agg {
   cred_t<WIDE> Smin;  // min fixed-point slo over running (valid iff R > 0)
   double min_d;       // the same as a double
   int64_t lens;       // sum of current_len over running
-  double inv;         // Neumaier sum of 1/slo over running, in order
-  bool inv_valid;
+  PySum pinv;         // Neumaier fold of 1/slo over running, in order (CPython sum state);
+  bool inv_valid;      // appends extend the fold exactly, removals invalidate it
 };
 
 // Greedy admission scan in queue order, speculative-parallel
@@ -254,7 +289,7 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
                            int64_t lg_adm, int64_t cap_adm, int64_t lg_rej, int64_t cap_rej) {
   const sl_cost& C = s.cost;
   int64_t n_run = R;
-  double inv = g.inv;
+  double inv = ps_result(g.pinv);  // plain adds below (:275); the fold is extended separately
   int64_t lens = g.lens;
   bool has_min = R > 0;
   double mind = g.min_d;
@@ -353,6 +388,7 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       }
       n_run += 1;
       inv = fadd_(inv, e.inv);  // plain float add, :275
+      ps_add(g.pinv, e.inv);    // next step's sum() over the running list
       lens += e.cur_len;
       if (lt_g) {
         mind = tp_g;
@@ -372,7 +408,7 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
   if (nadm) {
     g.min_d = mind;
     g.Smin = Smn;
-    g.inv_valid = false;  // the scan's plain adds are not the Neumaier sum
+    // the fold g.pinv was extended entry by entry (the scan's plain adds are not it)
   }
   return ok_cap;
 }
@@ -659,13 +695,13 @@ __device__ __forceinline__ bool block_steps(const Sim& s, const KArgs& a, bool h
     }
     if (W > 0) {  // every waiting request fails the admission test at the current state
       if (!g.inv_valid) {
-        g.inv = running_inv_sum<WIDE>(sl, R, lane, bc);
+        g.pinv = running_inv_sum<WIDE>(sl, R, lane, bc);
         g.inv_valid = true;
       }
       const double mind = g.min_d;
       const bool lt = w_tp < mind;
       const double minp = lt ? w_tp : mind;
-      const double V = fmul_(minp, fadd_(g.inv, w_ic));
+      const double V = fmul_(minp, fadd_(ps_result(g.pinv), w_ic));
       const double L = fdiv_((double)(g.lens + w_ln), (double)(R + 1));
       const double est = tpot_estimate(C, V, L, w_ps & 0x7fffffff);
       const double thr = r_only ? mind : minp;
@@ -794,24 +830,27 @@ __device__ __forceinline__ bool block_steps(const Sim& s, const KArgs& a, bool h
   return false;
 }
 
-template <bool WIDE>
+// HOT: compile-time specialisation for the sweep's common case -- scorpio with
+// both guards, no decision log -- so the hot kernel carries no baseline,
+// ablation or logging code (smaller instruction footprint, fewer registers).
+template <bool WIDE, bool HOT = false>
 __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_out, int si, int lane,
                          Slot<WIDE>* scr) {
   const int64_t n = s.n;
   const sl_cost& C = s.cost;
-  const bool scorpio = s.policy == SL_POLICY_SCORPIO;
-  const bool ttft_guard = (s.flags & SL_FLAG_TTFT_GUARD) != 0;
-  const bool tpot_guard = (s.flags & SL_FLAG_TPOT_GUARD) != 0;
+  const bool scorpio = HOT || s.policy == SL_POLICY_SCORPIO;
+  const bool ttft_guard = HOT || (s.flags & SL_FLAG_TTFT_GUARD) != 0;
+  const bool tpot_guard = HOT || (s.flags & SL_FLAG_TPOT_GUARD) != 0;
   const bool r_only = (s.flags & SL_FLAG_R_ONLY) != 0;
   const bool has_h = (s.flags & SL_FLAG_HAS_HORIZON) != 0;
   const bool sorted_ldf = scorpio && ttft_guard;
-  const bool sjf = s.policy == SL_POLICY_SJF;
+  const bool sjf = !HOT && s.policy == SL_POLICY_SJF;
   const bool credit = scorpio && tpot_guard;
-  const bool prio = !scorpio && (s.flags & SL_FLAG_PREFILL_PRIORITY);
+  const bool prio = !HOT && !scorpio && (s.flags & SL_FLAG_PREFILL_PRIORITY);
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
   if (has_out) init_outcomes(s, a, lane);
-  const bool logging = a.has_log && s.log_row >= 0;
+  const bool logging = !HOT && a.has_log && s.log_row >= 0;
   const int64_t lg_step0 = logging ? s.log_row * a.log.step_cap : 0;
   const int64_t lg_id0 = logging ? s.log_row * a.log.id_cap : 0;
   int64_t cur_adm = 0, cur_rej = 0, cur_bat = 0;
@@ -834,7 +873,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
   g.Smin = 0;
   g.min_d = 0.0;
   g.lens = 0;
-  g.inv = 0.0;
+  ps_init(g.pinv);
   g.inv_valid = true;
 
   double now = 0.0;
@@ -843,11 +882,17 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
   int W = 0, R = 0;
   int64_t step = 0, n_plans = 0, n_idle = 0, req_steps = 0;
   int status = SL_SIM_OK;
+  bool blocked = false;
+  double walk_until = -kInf;  // the walk rejects nothing while now < walk_until
+  const bool mono = C.alpha >= 0.0 && C.gamma >= 0.0 && C.epsilon >= 0.0;  // est monotone in L
   SL_PROF_DECL
 
   for (;;) {
-    if (next < n && next_t <= now)
+    if (next < n && next_t <= now) {
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
+      blocked = false;
+      walk_until = -kInf;  // an insertion can grow other items' prefixes
+    }
     SL_PROF_MARK(0)
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
 #if SL_QUIET_MODE == 0
@@ -895,28 +940,33 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     bool fits = true;
     if (W > 0) {
       if (scorpio) {
-        if (ttft_guard)
+        if (ttft_guard && !(now < walk_until))
           spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
-                    reinterpret_cast<double*>(scr));
+                    reinterpret_cast<double*>(scr), walk_until);
         SL_PROF_MARK(2)
         if (tpot_guard) {
-          if (W > 0) {
+          // `blocked`: every waiting request failed the admission test at a
+          // previous step and is feasible alone, and since then only `lens`
+          // has grown (no arrival, admission or retirement); the estimate is
+          // monotone in L, so the whole scan would admit and reject nothing.
+          if (W > 0 && !blocked) {
             if (!g.inv_valid) {
-              g.inv = running_inv_sum<WIDE>(sl, R, lane, reinterpret_cast<double*>(scr));
+              g.pinv = running_inv_sum<WIDE>(sl, R, lane, reinterpret_cast<double*>(scr));
               g.inv_valid = true;
             }
             SL_PROF_MARK(3)
             fits = spec_admit<WIDE>(s, a, has_out, W, R, sl, g, nadm, nrej, P, r_only, step, acc,
                                     lane, lg_adm, cap_adm, lg_rej, cap_rej);
+            blocked = mono && nadm == 0;
           }
         } else {
           fits = append_prefix<WIDE>(s, a, W, R, sl, g, W, nadm, P, step, acc, lane, lg_adm,
                                      cap_adm);
         }
       } else {
-        if (s.policy == SL_POLICY_EARLY_REJECT)
+        if (s.policy == SL_POLICY_EARLY_REJECT && !(now < walk_until))
           spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
-                    reinterpret_cast<double*>(scr));
+                    reinterpret_cast<double*>(scr), walk_until);
         int room = s.cap - R;
         int take = room > 0 ? min(room, W) : 0;
         if (take > 0)
@@ -937,6 +987,8 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     const bool decode = credit || !(prio && nadm > 0);
 #pragma unroll
     for (int k = 0; k < kSlots; ++k) {
+      bm[k] = 0u;
+      if (k > 0 && R0 <= 32 * k) break;
       const int j = 32 * k + lane;
       bool b = false;
       if (decode && j < R0) {
@@ -1078,7 +1130,10 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     for (int k = 0; k < kSlots; ++k)
       any_ret |= __any_sync(SL_FULL, 32 * k + lane < R && sl[k].rem <= 0);
     SL_PROF_MARK(6)
-    if (any_ret) retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
+    if (any_ret) {
+      retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
+      blocked = false;
+    }
     SL_PROF_COUNT(11, W > 0 && nadm == 0 && nrej == 0)
     SL_PROF_MARK(7)
     now = end;

@@ -612,10 +612,19 @@ __global__ void __launch_bounds__(128) sl_sim_kernel(const __grid_constant__ KAr
 // Fast kernel: running set in registers (sim_fast.cuh); hands off sims that
 // outgrow it or are flagged general-only.
 constexpr int kFastWarps = 4;
-#ifndef SL_FAST_MIN_BLOCKS
-#define SL_FAST_MIN_BLOCKS 1
+#ifndef SL_HOT_MIN_BLOCKS
+#define SL_HOT_MIN_BLOCKS 3  // 12 warps/SM for the hot kernel (<= 168 registers)
 #endif
-__global__ void __launch_bounds__(32 * kFastWarps, SL_FAST_MIN_BLOCKS) sl_sim_fast_kernel(
+__device__ __forceinline__ bool hot_eligible(const sl_sim& sp) {
+  const int f = SL_FLAG_TTFT_GUARD | SL_FLAG_TPOT_GUARD;
+  return sp.policy == SL_POLICY_SCORPIO && (sp.flags & f) == f &&
+         !(sp.flags & SL_FLAG_GENERAL_ONLY) && !sp.credit_wide;
+}
+
+// HOT = true: scorpio-with-both-guards sims only, no decision log (OUT: outcomes
+// requested); HOT = false: every other sim (all sims when a log is requested).
+template <bool HOT, bool OUT>
+__global__ void __launch_bounds__(32 * kFastWarps, HOT ? SL_HOT_MIN_BLOCKS : 1) sl_sim_fast_kernel(
     const __grid_constant__ KArgs a) {
   __shared__ Slot<false> scratch[kFastWarps][kRunCap];
   const int lane = threadIdx.x & 31;
@@ -623,18 +632,23 @@ __global__ void __launch_bounds__(32 * kFastWarps, SL_FAST_MIN_BLOCKS) sl_sim_fa
   Workspace ws = carve(a.ws_base, a.slots);
   for (;;) {
     int q = 0;
-    if (lane == 0) q = atomicAdd(ws.counter, 1);
+    if (lane == 0) q = atomicAdd(ws.counter + (HOT ? 0 : 2), 1);
     q = __shfl_sync(SL_FULL, q, 0);
     if (q >= a.n_sims) return;
     int si = a.order ? a.order[q] : q;
     const sl_sim& sp = a.sims[si];
+    const bool hot = hot_eligible(sp);
+    if (HOT ? !hot : (hot && !a.has_log)) continue;  // the other fast kernel's sim
     if ((sp.flags & SL_FLAG_GENERAL_ONLY) || sp.credit_wide) {  // 128-bit credits: general
       if (lane == 0) a.results[si].status = SL_SIM_CAPACITY;
       continue;
     }
     Sim s = make_sim(a, ws, si);
-    bool has_out = a.has_out && s.out_off >= 0;
-    run_fast<false>(s, a, has_out, si, lane, scratch[warp]);
+    if (HOT) {
+      run_fast<false, true>(s, a, OUT && s.out_off >= 0, si, lane, scratch[warp]);
+    } else {
+      run_fast<false, false>(s, a, a.has_out && s.out_off >= 0, si, lane, scratch[warp]);
+    }
   }
 }
 
@@ -673,7 +687,7 @@ int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_
   return SL_OK;
 }
 
-int sl_run_batch_launches(void) { return 2; }
+int sl_run_batch_launches(void) { return 3; }  // hot fast + generic fast + general handoff
 
 #ifdef SL_PHASE_PROF
 // Profiling builds only: per-sim phase cycles / counts of the fast kernel.
@@ -754,8 +768,17 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
     return (unsigned)(blocks < max_blocks ? blocks : max_blocks);
   };
   if (mode == SL_MODE_AUTO) {
-    sl_sim_fast_kernel<<<grid_for((const void*)sl_sim_fast_kernel, 32 * kFastWarps),
-                         32 * kFastWarps, 0, st>>>(a);
+    if (!a.has_log) {
+      if (a.has_out)
+        sl_sim_fast_kernel<true, true><<<grid_for((const void*)sl_sim_fast_kernel<true, true>,
+                                                  32 * kFastWarps), 32 * kFastWarps, 0, st>>>(a);
+      else
+        sl_sim_fast_kernel<true, false><<<grid_for((const void*)sl_sim_fast_kernel<true, false>,
+                                                   32 * kFastWarps), 32 * kFastWarps, 0, st>>>(a);
+      if (cudaGetLastError() != cudaSuccess) return SL_ERR_CUDA;
+    }
+    sl_sim_fast_kernel<false, false><<<grid_for((const void*)sl_sim_fast_kernel<false, false>,
+                                                32 * kFastWarps), 32 * kFastWarps, 0, st>>>(a);
     if (cudaGetLastError() != cudaSuccess) return SL_ERR_CUDA;
   }
   sl_sim_kernel<<<grid_for((const void*)sl_sim_kernel, 128), 128, 0, st>>>(

@@ -102,7 +102,7 @@ __device__ __forceinline__ double tpot_estimate(const sl_cost& c, double V, doub
 __device__ __forceinline__ bool solo_ok(const sl_cost& c, double cand, double inv_cand,
                                         int32_t len, int32_t pred) {
   double V = fmul_(cand, fadd_(0.0, inv_cand));
-  double L = fdiv_(fadd_(0.0, (double)len), 1.0);
+  double L = (double)len;  // (0 + len) / 1 exactly
   return tpot_estimate(c, V, L, pred) <= cand;
 }
 
