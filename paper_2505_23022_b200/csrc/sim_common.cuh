@@ -271,7 +271,7 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
 struct Acc {
   uint64_t dig;      // committed digest partial
   uint64_t dig_rej;  // pending: rejections of the current plan (committed iff it has work)
-  int64_t completed, compliant, rej_ttft, rej_adm, ttft_viol, tpot_viol;
+  int32_t completed, compliant, rej_ttft, rej_adm, ttft_viol, tpot_viol;  // per-lane partials
 };
 
 __device__ __forceinline__ void write_result(const KArgs& a, int si, const Acc& acc, int status,
@@ -279,12 +279,13 @@ __device__ __forceinline__ void write_result(const KArgs& a, int si, const Acc& 
                                              int64_t n_idle, int64_t req_steps, double now,
                                              bool has_h, double horizon, int lane) {
   uint64_t dig = warp_sum_u64(acc.dig);
-  int64_t completed = warp_sum_i64(acc.completed);
-  int64_t compliant = warp_sum_i64(acc.compliant);
-  int64_t rj_t = warp_sum_i64(acc.rej_ttft);
-  int64_t rj_a = warp_sum_i64(acc.rej_adm);
-  int64_t tv = warp_sum_i64(acc.ttft_viol);
-  int64_t pv = warp_sum_i64(acc.tpot_viol);
+  // per-lane partial counts are < 2^31 and their sums <= n < 2^32
+  int64_t completed = __reduce_add_sync(SL_FULL, (unsigned)acc.completed);
+  int64_t compliant = __reduce_add_sync(SL_FULL, (unsigned)acc.compliant);
+  int64_t rj_t = __reduce_add_sync(SL_FULL, (unsigned)acc.rej_ttft);
+  int64_t rj_a = __reduce_add_sync(SL_FULL, (unsigned)acc.rej_adm);
+  int64_t tv = __reduce_add_sync(SL_FULL, (unsigned)acc.ttft_viol);
+  int64_t pv = __reduce_add_sync(SL_FULL, (unsigned)acc.tpot_viol);
   if (lane == 0) {
     sl_result res;
     res.status = status;

@@ -22,17 +22,12 @@ namespace sl {
 
 constexpr int kSlots = 2;
 constexpr int kRunCap = 32 * kSlots;
-#ifndef SL_QUIET_MODE
-#define SL_QUIET_MODE 0  // 0: serial quiet steps (default: best sweep throughput); 1: block steps
+#ifndef SL_QUIET_BLOCK_MIN
+#define SL_QUIET_BLOCK_MIN 33  // lookahead block when >= this many quiet steps may start (33: never;
+                               // the block code costs more icache than it saves in a sweep)
 #endif
-#ifndef SL_BLOCK_RMAX
-#define SL_BLOCK_RMAX 64
-#endif
-#ifndef SL_BLOCK_WMAX
-#define SL_BLOCK_WMAX 32
-#endif
-#ifndef SL_BLOCKED_MIN
-#define SL_BLOCKED_MIN 8  // min. block length bound for a blocked (waiting > 0) block
+#ifndef SL_QUIET_BLOCK_RMAX
+#define SL_QUIET_BLOCK_RMAX 4  // ... and at most this many running (rare retirements)
 #endif
 
 // Optional per-phase cycle accounting (profiling builds only: -DSL_PHASE_PROF,
@@ -61,15 +56,17 @@ __device__ unsigned long long sl_prof_cycles[kProfSims][kProfSlots];
 #define SL_PROF_WRITE(si)
 #endif
 
+// A running entry held in registers.  1/slo is recomputed from S when the
+// Neumaier fold has to be rebuilt, the first-token time lives in the
+// workspace (first_emit[idx]); the id is only read by the decision log.
 template <bool WIDE>
 struct Slot {
   cred_t<WIDE> N, S;  // credit numerator, fixed-point slo
-  double inv;         // 1 / tpot
-  double first;       // first-token time
   int64_t id;         // request id
   int32_t idx;        // request index in the trace
   int32_t cur_len;    // prompt_len + tokens_generated
   int32_t rem;        // true_output_len - tokens_generated
+  uint32_t hid;       // batch_hid(id), the digest's per-entry hash
 };
 
 // Conditional per-field moves (not `sl[pos >> 5] = e`, which would force the
@@ -78,9 +75,8 @@ template <bool WIDE>
 __device__ __forceinline__ void sel_slot(Slot<WIDE>& d, bool c, const Slot<WIDE>& e) {
   d.N = c ? e.N : d.N;
   d.S = c ? e.S : d.S;
-  d.inv = c ? e.inv : d.inv;
-  d.first = c ? e.first : d.first;
   d.id = c ? e.id : d.id;
+  d.hid = c ? e.hid : d.hid;
   d.idx = c ? e.idx : d.idx;
   d.cur_len = c ? e.cur_len : d.cur_len;
   d.rem = c ? e.rem : d.rem;
@@ -98,15 +94,16 @@ __device__ __forceinline__ void put_slot(Slot<WIDE> (&sl)[kSlots], int pos, cons
 // Neumaier sum of 1/slo over the running set in order; the serial chain reads
 // its operands from a per-warp smem broadcast buffer `bc` (32 doubles).
 template <bool WIDE>
-__device__ __forceinline__ PySum running_inv_sum(const Slot<WIDE> (&sl)[kSlots], int R, int lane,
-                                                 double* bc) {
+__device__ __forceinline__ PySum running_inv_sum(const Sim& s, const Slot<WIDE> (&sl)[kSlots],
+                                                 int R, int lane, double* bc) {
   PySum ps;
   ps_init(ps);
 #pragma unroll
   for (int k = 0; k < kSlots; ++k) {
     const int cnt = min(32, R - 32 * k);
     if (cnt <= 0) break;
-    bc[lane] = sl[k].inv;
+    // 1.0 / tpot: S * 2^E is tpot exactly, so this is the WRec's inv bit for bit
+    if (32 * k + lane < R) bc[lane] = fdiv_(1.0, fixed_to_double<WIDE>(sl[k].S, s.pow2E));
     __syncwarp();
     for (int t = 0; t < cnt; ++t) ps_add(ps, bc[t]);
     __syncwarp();
@@ -124,25 +121,6 @@ __device__ __forceinline__ cred_t<WIDE> running_min(const Slot<WIDE> (&sl)[kSlot
   return warp_min_cred<WIDE>(m);
 }
 
-// Time up to which the walk provably rejects nothing: item j passed at `now`
-// with prefix bound U (est0 = fl(fl(fl(now - arr) + U) + pf) <= ttft); its est
-// at a later now1 (prefix <= U: prefixes only shrink until an insertion) stays
-// <= ttft while now1 - now < sigma - m, sigma = fl(ttft - est0) and
-// m = 2^-40 * 2 * (now + U + pf + sigma) >> the <= 8u relative rounding error
-// of the three-op chain evaluated at now and now1.
-__device__ __forceinline__ double walk_pass_until(double now, double U, double pf, double tt,
-                                                  double est0) {
-  const double sig = fsub_(tt, est0);
-  const double m = fmul_(1.8189894035458565e-12, fadd_(fadd_(fadd_(now, U), pf), sig));  // 2^-39 *
-  return fsub_(fadd_(now, sig), m);
-}
-
-__device__ __forceinline__ double warp_min_d(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(SL_FULL, v, o));
-  return v;
-}
-
 // TTFT prefix walk over wl[0, W) in list order (ttft_guard sched_scorpio.py:196-205;
 // early_reject sched_baselines.py:95-103).
 //  1. Certified pass: an upper bound U_j of the sequential prefix (warp scan in
@@ -153,17 +131,12 @@ __device__ __forceinline__ double warp_min_d(double v) {
 //  2. Otherwise the exact walk, speculative-parallel: the sequential chain
 //     assuming all undecided items are kept, lane-parallel tests, ballot for the
 //     first rejection, restart after it.
-// `until` receives the time before which the walk over the remaining queue
-// rejects nothing (walk_pass_until), valid until the next insertion.
 __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W,
                                           int& nrej, double now, int64_t step, Acc& acc, int lane,
-                                          int64_t lg_rej, int64_t cap_rej, double* bc,
-                                          double& until) {
-  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+                                          int64_t lg_rej, int64_t cap_rej, double* bc) {
   if (W < (1 << 20)) {
     const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
     double U = 0.0;
-    double tmin = kInf;
     bool all_ok = true;
     for (int c0 = 0; c0 < W && all_ok; c0 += 32) {
       const int j = c0 + lane;
@@ -184,19 +157,13 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
       double excl = __shfl_up_sync(SL_FULL, v, 1);
       if (lane == 0) excl = 0.0;
       const double Uj = fmul_(fadd_(U, excl), inflate);
-      const double est0 = fadd_(fadd_(e, Uj), pf);
-      all_ok = __all_sync(SL_FULL, !valid || est0 <= tt);
-      if (valid) tmin = fmin(tmin, walk_pass_until(now, Uj, pf, tt, est0));
+      all_ok = __all_sync(SL_FULL, !valid || fadd_(fadd_(e, Uj), pf) <= tt);
       U = fmul_(fadd_(U, __shfl_sync(SL_FULL, v, 31)), inflate);
     }
-    if (all_ok) {
-      until = warp_min_d(tmin);
-      return;
-    }
+    if (all_ok) return;
   }
   double* pre = bc + 32;
   double prefix = 0.0;
-  double tmin = kInf;
   int kept = 0;
   for (int c0 = 0; c0 < W; c0 += 32) {
     const int j = c0 + lane;
@@ -238,10 +205,6 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     }
     const bool r_ = valid && ((rejm >> lane) & 1u);
     const bool keep = valid && !r_;
-    if (keep) {
-      const double mine = pre[lane];
-      tmin = fmin(tmin, walk_pass_until(now, mine, pf, tt, fadd_(fadd_(e, mine), pf)));
-    }
     const unsigned km = __ballot_sync(SL_FULL, keep);
     __syncwarp();
     if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
@@ -258,7 +221,6 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     nrej += __popc(rejm);
   }
   W = kept;
-  until = warp_min_d(tmin);
 }
 
 // Position of the n-th (1-based) set bit of x; requires 1 <= n <= popc(x).
@@ -360,9 +322,9 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       Slot<WIDE> e;
       e.N = 0;
       e.S = shfl_cred<WIDE>(Sc, gl);
-      e.inv = bcast(ic, gl);
-      e.first = 0.0;
       e.id = bcast(rid, gl);
+      e.hid = batch_hid((uint64_t)e.id);
+      const double e_inv = bcast(ic, gl);
       e.idx = bcast(idx, gl);
       e.cur_len = bcast(ln, gl);
       e.rem = bcast(tout, gl);
@@ -387,8 +349,8 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
         if (lg_adm >= 0 && nadm < cap_adm) a.log.adm_ids[lg_adm + nadm] = e.id;
       }
       n_run += 1;
-      inv = fadd_(inv, e.inv);  // plain float add, :275
-      ps_add(g.pinv, e.inv);    // next step's sum() over the running list
+      inv = fadd_(inv, e_inv);  // plain float add, :275
+      ps_add(g.pinv, e_inv);    // next step's sum() over the running list
       lens += e.cur_len;
       if (lt_g) {
         mind = tp_g;
@@ -436,9 +398,8 @@ __device__ __forceinline__ bool append_prefix(const Sim& s, const KArgs& a, int&
         e.S = ((unsigned __int128)s.wShi[idx] << 64) | w.S;
       else
         e.S = w.S;
-      e.inv = w.inv;
-      e.first = 0.0;
       e.id = s.id[idx];
+      e.hid = batch_hid((uint64_t)e.id);
       e.idx = idx;
       e.cur_len = w.prompt;
       e.rem = s.true_out[idx];
@@ -450,9 +411,8 @@ __device__ __forceinline__ bool append_prefix(const Sim& s, const KArgs& a, int&
       Slot<WIDE> x;
       x.N = 0;
       x.S = shfl_cred<WIDE>(e.S, t);
-      x.inv = bcast(e.inv, t);
-      x.first = 0.0;
       x.id = bcast(e.id, t);
+      x.hid = bcast(e.hid, t);
       x.idx = bcast(e.idx, t);
       x.cur_len = bcast(e.cur_len, t);
       x.rem = bcast(e.rem, t);
@@ -504,7 +464,7 @@ __device__ __forceinline__ void retire(const Sim& s, const KArgs& a, bool has_ou
     if (ret) {
       const int idx = sl[k].idx;
       const WRec& w = s.wr[idx];
-      const double first = sl[k].first;
+      const double first = s.first_emit[idx];
       const int32_t tout = s.true_out[idx];
       const double tpot = tout == 1 ? 0.0 : fdiv_(fsub_(end, first), (double)(tout - 1));
       const double ttft = fsub_(first, w.arr);
@@ -539,24 +499,145 @@ __device__ __forceinline__ void retire(const Sim& s, const KArgs& a, bool has_ou
   }
 }
 
-// Serial quiet steps (nothing waiting, <= 32 running, credit batching, no
-// log): the general step restricted to that case, one step per iteration.
-// The digest items of the steps are deferred and hashed lane-parallel, 32
-// steps per pass (lane j keeps step base+j).
+// One lookahead block of quiet steps (R <= 32, nothing waiting): within it the
+// membership is fixed, so every decision is a function of integer state:
+//  A. lane e runs its entry's credit recurrence (select_batch,
+//     sched_scorpio.py:171-179) for up to 32 steps: bit j of `bits` = entry
+//     batched at step j; the first retirement (the rem-th set bit) caps the block;
+//  B. per step j: batch size, length sum and id-hash sum (ballot + redux) -> lane j;
+//  C. lane j evaluates its step's itl() (simengine.py:233-238) -- all in
+//     parallel -- and only the clock now_{j+1} = now_j + d_j, which IEEE
+//     rounding makes order dependent, stays a serial chain (one DADD per
+//     step); the block ends before the first step whose start time sees an
+//     arrival or the horizon;
+//  D. the K executed steps are committed: credits in closed form (exact mod
+//     2^w, the true value lies in [0, S)), digest items (lane j: step j),
+//     retirement.
+// The empty prefill sum is 0 and now + 0 == now; the strictest entry always
+// batches, so every step has work.
 template <bool WIDE>
-__device__ __forceinline__ void quiet_serial(const Sim& s, const KArgs& a, bool has_out,
-                                             Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
-                                             double& now, int64_t& step, int64_t& n_plans,
-                                             int64_t& req_steps, double next_t, bool has_h,
-                                             Acc& acc, int lane, Slot<WIDE>* scr) {
+__device__ __forceinline__ bool quiet_block(const Sim& s, const KArgs& a, bool has_out,
+                                            Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
+                                            double& now, int64_t& step, int64_t& n_plans,
+                                            int64_t& req_steps, double next_t, double horizon,
+                                            int jcap, Acc& acc, int lane, Slot<WIDE>* scr) {
+  const sl_cost& C = s.cost;
+  double* dur = reinterpret_cast<double*>(scr);  // [32] step durations
+  double* clk = dur + 32;                         // [33] step start times + block end
+  const bool live = lane < R;
+  // A. credit recurrence
+  const cred_t<WIDE> M = g.Smin, S = sl[0].S;
+  cred_t<WIDE> N = sl[0].N;
+  unsigned bits = 0u;
+  for (int j = 0; j < jcap; ++j) {
+    N += M;
+    const bool b = N >= S;
+    N = b ? N - S : N;
+    bits |= (unsigned)b << j;
+  }
+  bits = live ? bits : 0u;
+  const unsigned rj = (live && sl[0].rem <= __popc(bits)) ? nth_set_bit(bits, sl[0].rem) : 32u;
+  const int jmax = min(jcap, (int)__reduce_min_sync(SL_FULL, rj) + 1);
+  // B. per-step batch size, length sum, id-hash sum -> lane j
+  int my_nb = 0;
+  unsigned my_blen = 0, my_bh = 0;
+  {
+    unsigned cl = live ? (unsigned)sl[0].cur_len : 0u;
+    const unsigned h = sl[0].hid;
+    for (int j = 0; j < jmax; ++j) {
+      const bool b = (bits >> j) & 1u;
+      const int nb = __popc(__ballot_sync(SL_FULL, b));
+      const unsigned bl = __reduce_add_sync(SL_FULL, b ? cl : 0u);
+      const unsigned bh = __reduce_add_sync(SL_FULL, b ? h : 0u);
+      cl += b;
+      if (lane == j) {
+        my_nb = nb;
+        my_blen = bl;
+        my_bh = bh;
+      }
+    }
+  }
+  // C. durations in parallel, the clock serially
+  if (lane < jmax) dur[lane] = itl(C, my_nb, fdiv_((double)my_blen, (double)my_nb));
+  __syncwarp();
+  {
+    double t = now;
+    for (int j = 0; j < jmax; ++j) {
+      if (lane == 0) clk[j] = t;
+      t = fadd_(t, dur[j]);
+    }
+    if (lane == 0) clk[jmax] = t;
+  }
+  __syncwarp();
+  const double my_start = clk[lane];
+  const double my_end = clk[lane + 1];
+  __syncwarp();
+  const unsigned runm = __ballot_sync(SL_FULL, lane < jmax && next_t > my_start && my_start < horizon);
+  const int K = (~runm == 0u) ? 32 : __ffs(~runm) - 1;  // >= 1: step 0 is quiet
+  // D. commit steps [0, K)
+  const int c = __popc(bits & (K == 32 ? ~0u : ((1u << K) - 1u)));
+  if (live) {
+    sl[0].N = sl[0].N + (cred_t<WIDE>)K * M - (cred_t<WIDE>)c * S;
+    sl[0].cur_len += c;
+    sl[0].rem -= c;
+  }
+  g.lens += __reduce_add_sync(SL_FULL, (unsigned)c);
+  n_plans += K;
+  req_steps += (int64_t)K * R;
+  if (lane < K)
+    acc.dig += digest_item((uint64_t)(step + lane), 2, (uint32_t)my_nb, my_bh) +
+               digest_item((uint64_t)(step + lane), 3, 0, (uint64_t)__double_as_longlong(my_end));
+  now = __shfl_sync(SL_FULL, my_end, K - 1);
+  step += K;
+  return __any_sync(SL_FULL, live && sl[0].rem <= 0);  // retirement due at `now`, step - 1
+}
+
+// Quiet steps (nothing waiting, <= 32 running, credit batching, no log): the
+// general step restricted to that case.  Where at least SL_QUIET_BLOCK_MIN steps
+// can start before the next arrival (bound below) it runs lookahead blocks
+// (quiet_block), otherwise one step per iteration, whose digest items are
+// deferred and hashed lane-parallel, 32 steps per pass (lane j keeps step base+j).
+// Returns true when entries retire at the end of the last step (at `now`, step
+// index `step - 1`): the caller runs retire() -- its one call site, which keeps
+// the hot instruction footprint small.
+template <bool WIDE>
+__device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool has_out,
+                                            Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
+                                            double& now, int64_t& step, int64_t& n_plans,
+                                            int64_t& req_steps, double next_t, bool has_h,
+                                            Acc& acc, int lane, Slot<WIDE>* scr) {
   const sl_cost& C = s.cost;
   const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
+  // itl is monotone in B and L for non-negative coefficients: every step then
+  // lasts >= itl(1, min current length), bounding the steps before `stop`
+  const bool mono_itl = C.alpha >= 0.0 && C.beta >= 0.0 && C.gamma >= 0.0 && C.delta > 0.0;
   int64_t base = step;
   uint64_t end_bits = 0;
   uint32_t d_nb = 0, d_bh = 0;
   bool have = false;
-  uint32_t hh = batch_hid((uint64_t)sl[0].id);
+  bool recheck = true;
+  int jcap = 0;
+  uint32_t hh = sl[0].hid;
   while (R > 0 && R <= 32 && next_t > now && now < horizon) {
+    if (SL_QUIET_BLOCK_MIN <= 32 && recheck && mono_itl) {
+      recheck = false;
+      const unsigned mlen = __reduce_min_sync(SL_FULL, lane < R ? (unsigned)sl[0].cur_len : ~0u);
+      const double span = fsub_(fmin(next_t, horizon), now);
+      const double dmin = itl(C, 1, (double)mlen);
+      jcap = span < 31.0 * dmin ? 1 + (int)(span / dmin) : 32;
+    }
+    if (jcap >= SL_QUIET_BLOCK_MIN && R <= SL_QUIET_BLOCK_RMAX) {
+      if (have)
+        acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
+                   digest_item((uint64_t)(base + lane), 3, 0, end_bits);
+      have = false;
+      if (quiet_block<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t,
+                            horizon, jcap, acc, lane, scr))
+        return true;
+      base = step;
+      recheck = true;
+      continue;
+    }
     ++n_plans;
     req_steps += R;
     const bool live = lane < R;
@@ -584,12 +665,10 @@ __device__ __forceinline__ void quiet_serial(const Sim& s, const KArgs& a, bool 
       d_bh = bh;
       have = true;
     }
-    if (__any_sync(SL_FULL, live && sl[0].rem <= 0)) {
-      retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
-      hh = batch_hid((uint64_t)sl[0].id);
-    }
+    const bool ret = __any_sync(SL_FULL, live && sl[0].rem <= 0);
     now = end;
     ++step;
+    if (ret) break;
     if (step - base == 32) {
       if (have)
         acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
@@ -601,233 +680,7 @@ __device__ __forceinline__ void quiet_serial(const Sim& s, const KArgs& a, bool 
   if (have)
     acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
                digest_item((uint64_t)(base + lane), 3, 0, end_bits);
-}
-
-// Block steps: runs of consecutive scheduler steps in which the running set
-// does not change membership and no waiting request is admitted or rejected.
-// Two kinds qualify (credit batching, no decision log, <= 64 running):
-//  * quiet steps -- nothing waiting (~64% of the steps of a config-3 sweep);
-//  * blocked steps -- 1..32 waiting requests, every one feasible alone
-//    (solo_ok) and failing the admission test against the current running
-//    aggregates (_admission_math, sched_scorpio.py:83-114).  With membership
-//    fixed only `lens` changes, and it only grows, so the estimate (monotone
-//    in L for non-negative alpha/gamma/epsilon) keeps failing: the scan
-//    (sched_scorpio.py:234-294) admits and rejects nothing.  The TTFT walk
-//    (:196-205) is monotone in `now`, so the first step at which it would
-//    reject an item is found by bisection over the block's clock; the block
-//    ends before it.  (~22% of the steps.)
-// In both, a step's duration depends only on integer state (the empty
-// prefill sum is 0 and now + 0 == now; the strictest entry always batches):
-//  A. lane e runs its entries' credit recurrences (select_batch,
-//     sched_scorpio.py:171-179) for up to 32 steps: bit j of `bits` = entry
-//     batched at step j; the first retirement (the rem-th set bit) caps the block;
-//  B. per step j: batch size, the sum of current lengths and the batch id hash
-//     (ballot + redux), delivered to lane j;
-//  C. lane j evaluates its step's itl() (simengine.py:233-238) -- all 32 in
-//     parallel -- and only the clock now_{j+1} = now_j + d_j, which IEEE
-//     rounding makes order dependent, stays a serial chain (one DADD per
-//     step); the block ends before the first step whose start time sees an
-//     arrival (or the horizon) or at which the walk would reject;
-//  D. the K executed steps are committed: credits in closed form (exact mod
-//     2^w, the true value lies in [0, S)), digest items (lane j: step j),
-//     retirement.
-// Returns true when the next step must be a general step at the same `now`
-// (a waiting request would be admitted or rejected); false when the loop
-// ended on an arrival, the horizon, or the running-set size.
-template <bool WIDE>
-__device__ __forceinline__ bool block_steps(const Sim& s, const KArgs& a, bool has_out,
-                                            Slot<WIDE> (&sl)[kSlots], int& R, const int W,
-                                            Agg<WIDE>& g, double& now, int64_t& step,
-                                            int64_t& n_plans, int64_t& req_steps, double next_t,
-                                            bool has_h, bool walk, bool r_only, Acc& acc,
-                                            int lane, Slot<WIDE>* scr) {
-  const sl_cost& C = s.cost;
-  const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
-  double* bc = reinterpret_cast<double*>(scr);
-  double* dur = bc;        // [32] step durations
-  double* clk = bc + 32;   // [33] step start times, clk[jmax] = end of the block
-  // waiting requests (lane i = queue position i), fixed for the whole call
-  const bool wv = lane < W;
-  double w_arr = 0.0, w_pf = 0.0, w_tt = 0.0, w_pre = 0.0, w_tp = 0.0, w_ic = 0.0;
-  int32_t w_ln = 0, w_ps = 0;
-  if (W > 0 && !(C.alpha >= 0.0 && C.gamma >= 0.0 && C.epsilon >= 0.0)) return true;
-  bool wloaded = false;
-  while (R > 0 && R <= 64 && next_t > now && now < horizon) {
-    const bool two = R > 32;
-    const bool live0 = lane < R, live1 = 32 + lane < R;
-    // Block length cap (any cap is exact; it only sizes the work): every step
-    // lasts at least itl(1, min current length) when the coefficients are
-    // non-negative (itl is then monotone in B and L), so at most
-    // (stop - now) / dmin + 1 steps start before the next arrival / horizon.
-    int jcap = 32;
-    if (C.alpha >= 0.0 && C.beta >= 0.0 && C.gamma >= 0.0 && C.delta > 0.0) {
-      unsigned ml = live0 ? (unsigned)sl[0].cur_len : ~0u;
-      if (live1) ml = min(ml, (unsigned)sl[1].cur_len);
-      const unsigned mlen = __reduce_min_sync(SL_FULL, ml);
-      const double dmin = itl(C, 1, (double)mlen);
-      const double span = fsub_(fmin(next_t, horizon), now);
-      if (span < 31.0 * dmin) jcap = 1 + (int)(span / dmin);
-    }
-    if (W > 0 && jcap < SL_BLOCKED_MIN) return true;  // too short to pay for itself
-    if (W > 0 && !wloaded) {  // load the waiting requests once per call
-      wloaded = true;
-      if (wv) {
-        const WRec& w = s.wr[s.wl[lane]];
-        w_arr = w.arr;
-        w_pf = w.prefill;
-        w_tt = w.ttft;
-        w_tp = w.tpot;
-        w_ic = w.inv;
-        w_ln = w.prompt;
-        w_ps = w.pred_solo;
-      }
-      if (!__all_sync(SL_FULL, !wv || (w_ps & (int32_t)0x80000000) != 0)) return true;
-      if (walk) {  // exact sequential prefix of the walk (nothing is rejected in a block)
-        dur[lane] = w_pf;
-        __syncwarp();
-        double t = 0.0;
-        for (int i = 0; i < W; ++i) {
-          if (lane == i) w_pre = t;
-          t = fadd_(t, dur[i]);
-        }
-        __syncwarp();
-      }
-    }
-    if (W > 0) {  // every waiting request fails the admission test at the current state
-      if (!g.inv_valid) {
-        g.pinv = running_inv_sum<WIDE>(sl, R, lane, bc);
-        g.inv_valid = true;
-      }
-      const double mind = g.min_d;
-      const bool lt = w_tp < mind;
-      const double minp = lt ? w_tp : mind;
-      const double V = fmul_(minp, fadd_(ps_result(g.pinv), w_ic));
-      const double L = fdiv_((double)(g.lens + w_ln), (double)(R + 1));
-      const double est = tpot_estimate(C, V, L, w_ps & 0x7fffffff);
-      const double thr = r_only ? mind : minp;
-      if (__any_sync(SL_FULL, wv && est <= thr)) return true;
-    }
-    // A. credit recurrences for jcap steps (all 32 when jcap == 32)
-    const cred_t<WIDE> M = g.Smin;
-    unsigned bits[kSlots];
-#pragma unroll
-    for (int k = 0; k < kSlots; ++k) {
-      bits[k] = 0u;
-      if (k == 1 && !two) break;
-      const cred_t<WIDE> S = sl[k].S;
-      cred_t<WIDE> N = sl[k].N;
-      if (jcap == 32) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          N += M;
-          const bool b = N >= S;
-          N = b ? N - S : N;
-          bits[k] |= (unsigned)b << j;
-        }
-      } else {
-        for (int j = 0; j < jcap; ++j) {
-          N += M;
-          const bool b = N >= S;
-          N = b ? N - S : N;
-          bits[k] |= (unsigned)b << j;
-        }
-      }
-    }
-    bits[0] = live0 ? bits[0] : 0u;
-    if (kSlots > 1) bits[1] = live1 ? bits[1] : 0u;
-    unsigned rj = (live0 && sl[0].rem <= __popc(bits[0])) ? nth_set_bit(bits[0], sl[0].rem) : 32u;
-    if (live1 && sl[1].rem <= __popc(bits[1])) rj = min(rj, nth_set_bit(bits[1], sl[1].rem));
-    const int jmax = min(jcap, (int)__reduce_min_sync(SL_FULL, rj) + 1);
-    // B. batch size, length sum and id-hash sum of step j -> lane j
-    int my_nb = 0;
-    unsigned my_blen = 0, my_bh = 0;
-    {
-      unsigned cl0 = live0 ? (unsigned)sl[0].cur_len : 0u;
-      unsigned cl1 = live1 ? (unsigned)sl[1].cur_len : 0u;
-      const unsigned h0 = batch_hid((uint64_t)sl[0].id);
-      const unsigned h1 = two ? batch_hid((uint64_t)sl[1].id) : 0u;
-      for (int j = 0; j < jmax; ++j) {
-        const bool b0 = (bits[0] >> j) & 1u;
-        const bool b1 = (bits[1] >> j) & 1u;
-        const int nb = (int)__reduce_add_sync(SL_FULL, (unsigned)b0 + (unsigned)b1);
-        const unsigned bl = __reduce_add_sync(SL_FULL, (b0 ? cl0 : 0u) + (b1 ? cl1 : 0u));
-        const unsigned bh = __reduce_add_sync(SL_FULL, (b0 ? h0 : 0u) + (b1 ? h1 : 0u));
-        cl0 += b0;
-        cl1 += b1;
-        if (lane == j) {
-          my_nb = nb;
-          my_blen = bl;
-          my_bh = bh;
-        }
-      }
-    }
-    // C. step durations in parallel; the clock chain serially
-    if (lane < jmax) dur[lane] = itl(C, my_nb, fdiv_((double)my_blen, (double)my_nb));
-    __syncwarp();
-    {
-      double t = now;
-      for (int j = 0; j < jmax; ++j) {
-        if (lane == 0) clk[j] = t;
-        t = fadd_(t, dur[j]);
-      }
-      if (lane == 0) clk[jmax] = t;
-    }
-    __syncwarp();
-    const double my_start = clk[lane];
-    const double my_end = clk[lane + 1];
-    // first step at which the walk would reject a waiting request (bisection;
-    // est is monotone in now)
-    int jw = 32;
-    if (W > 0 && walk) {
-      int lo = 0, hi = jmax;  // first j in [0, jmax) with est(clk[j]) > ttft, else jmax
-      if (wv) {
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (fadd_(fadd_(fsub_(clk[mid], w_arr), w_pre), w_pf) > w_tt)
-            hi = mid;
-          else
-            lo = mid + 1;
-        }
-      } else {
-        lo = jmax;
-      }
-      jw = (int)__reduce_min_sync(SL_FULL, (unsigned)lo);
-    }
-    __syncwarp();
-    const unsigned runm =
-        __ballot_sync(SL_FULL, lane < jmax && lane < jw && next_t > my_start && my_start < horizon);
-    const int K = (~runm == 0u) ? 32 : __ffs(~runm) - 1;
-    if (K == 0) return true;  // the walk rejects at this very step
-    // D. commit steps [0, K)
-    const unsigned km = K == 32 ? ~0u : ((1u << K) - 1u);
-    int csum = 0;
-#pragma unroll
-    for (int k = 0; k < kSlots; ++k) {
-      const bool live = k == 0 ? live0 : live1;
-      const int c = __popc(bits[k] & km);
-      if (live) {
-        sl[k].N = sl[k].N + (cred_t<WIDE>)K * M - (cred_t<WIDE>)c * sl[k].S;
-        sl[k].cur_len += c;
-        sl[k].rem -= c;
-      }
-      csum += c;
-    }
-    g.lens += __reduce_add_sync(SL_FULL, (unsigned)csum);
-    n_plans += K;
-    req_steps += (int64_t)K * (R + W);
-    if (lane < K)
-      acc.dig += digest_item((uint64_t)(step + lane), 2, (uint32_t)my_nb, my_bh) +
-                 digest_item((uint64_t)(step + lane), 3, 0, (uint64_t)__double_as_longlong(my_end));
-    const double end = __shfl_sync(SL_FULL, my_end, K - 1);
-    step += K;
-    __syncwarp();
-    if (__any_sync(SL_FULL, (live0 && sl[0].rem <= 0) || (live1 && sl[1].rem <= 0)))
-      retire<WIDE>(s, a, has_out, sl, R, g, end, step - 1, acc, lane, scr);
-    now = end;
-    // walk rejection due at the next step, no arrival pending: a general step follows
-    if (K == jw && next_t > now && now < horizon) return true;
-  }
-  return false;
+  return R > 0 && __any_sync(SL_FULL, lane < R && sl[0].rem <= 0);
 }
 
 // HOT: compile-time specialisation for the sweep's common case -- scorpio with
@@ -862,9 +715,8 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
   for (int k = 0; k < kSlots; ++k) {
     sl[k].N = 0;
     sl[k].S = 0;
-    sl[k].inv = 0.0;
-    sl[k].first = 0.0;
     sl[k].id = 0;
+    sl[k].hid = 0;
     sl[k].idx = 0;
     sl[k].cur_len = 0;
     sl[k].rem = 0;
@@ -883,7 +735,6 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
   int64_t step = 0, n_plans = 0, n_idle = 0, req_steps = 0;
   int status = SL_SIM_OK;
   bool blocked = false;
-  double walk_until = -kInf;  // the walk rejects nothing while now < walk_until
   const bool mono = C.alpha >= 0.0 && C.gamma >= 0.0 && C.epsilon >= 0.0;  // est monotone in L
   SL_PROF_DECL
 
@@ -891,33 +742,18 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     if (next < n && next_t <= now) {
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
       blocked = false;
-      walk_until = -kInf;  // an insertion can grow other items' prefixes
     }
     SL_PROF_MARK(0)
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
-#if SL_QUIET_MODE == 0
+    bool ret;  // entries retire at the end of step `step - 1` (at `now`)
     if (W == 0 && credit && !logging && R > 0 && R <= 32) {
       SL_PROF_COUNT(9, 1)
       SL_PROF_COUNT(10, -step)
-      quiet_serial<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t, has_h,
-                         acc, lane, scr);
+      ret = quiet_steps<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t,
+                              has_h, acc, lane, scr);
       SL_PROF_COUNT(10, step)
       SL_PROF_MARK(1)
-      continue;
-    }
-    if (false) {
-#else
-    if (credit && !logging && R > 0 && R <= SL_BLOCK_RMAX && W <= SL_BLOCK_WMAX) {
-#endif
-      SL_PROF_COUNT(9, 1)
-      SL_PROF_COUNT(10, -step)
-      const bool general = block_steps<WIDE>(s, a, has_out, sl, R, W, g, now, step, n_plans,
-                                             req_steps, next_t, has_h, ttft_guard, r_only, acc,
-                                             lane, scr);
-      SL_PROF_COUNT(10, step)
-      SL_PROF_MARK(1)
-      if (!general) continue;
-    }
+    } else {
     SL_PROF_COUNT(8, 1)
     SL_PROF_COUNT(12, W == 0)
     SL_PROF_COUNT(13, R > 32)
@@ -940,9 +776,9 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     bool fits = true;
     if (W > 0) {
       if (scorpio) {
-        if (ttft_guard && !(now < walk_until))
+        if (ttft_guard)
           spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
-                    reinterpret_cast<double*>(scr), walk_until);
+                    reinterpret_cast<double*>(scr));
         SL_PROF_MARK(2)
         if (tpot_guard) {
           // `blocked`: every waiting request failed the admission test at a
@@ -951,7 +787,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
           // monotone in L, so the whole scan would admit and reject nothing.
           if (W > 0 && !blocked) {
             if (!g.inv_valid) {
-              g.pinv = running_inv_sum<WIDE>(sl, R, lane, reinterpret_cast<double*>(scr));
+              g.pinv = running_inv_sum<WIDE>(s, sl, R, lane, reinterpret_cast<double*>(scr));
               g.inv_valid = true;
             }
             SL_PROF_MARK(3)
@@ -964,9 +800,9 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
                                      cap_adm);
         }
       } else {
-        if (s.policy == SL_POLICY_EARLY_REJECT && !(now < walk_until))
+        if (s.policy == SL_POLICY_EARLY_REJECT)
           spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
-                    reinterpret_cast<double*>(scr), walk_until);
+                    reinterpret_cast<double*>(scr));
         int room = s.cap - R;
         int take = room > 0 ? min(room, W) : 0;
         if (take > 0)
@@ -1002,7 +838,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       }
       bm[k] = __ballot_sync(SL_FULL, b);
       blen += __reduce_add_sync(SL_FULL, b ? (unsigned)sl[k].cur_len : 0u);
-      bhash += __reduce_add_sync(SL_FULL, b ? batch_hid((uint64_t)sl[k].id) : 0u);
+      bhash += __reduce_add_sync(SL_FULL, b ? sl[k].hid : 0u);
       if (b) {
         int pos = nb + __popc(bm[k] & lanemask_lt());
         if (lg_bat >= 0 && pos < cap_bat) a.log.batch_ids[lg_bat + pos] = sl[k].id;
@@ -1120,7 +956,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
         if (j >= R0 && j < R) {
           sl[k].cur_len += 1;
           sl[k].rem -= 1;
-          sl[k].first = end;
+          s.first_emit[sl[k].idx] = end;
         }
       }
       g.lens += nadm;
@@ -1130,14 +966,16 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     for (int k = 0; k < kSlots; ++k)
       any_ret |= __any_sync(SL_FULL, 32 * k + lane < R && sl[k].rem <= 0);
     SL_PROF_MARK(6)
-    if (any_ret) {
-      retire<WIDE>(s, a, has_out, sl, R, g, end, step, acc, lane, scr);
-      blocked = false;
-    }
     SL_PROF_COUNT(11, W > 0 && nadm == 0 && nrej == 0)
-    SL_PROF_MARK(7)
     now = end;
     ++step;
+    ret = any_ret;
+    }  // general step
+    if (ret) {  // the one retire() call site
+      retire<WIDE>(s, a, has_out, sl, R, g, now, step - 1, acc, lane, scr);
+      blocked = false;
+    }
+    SL_PROF_MARK(7)
   }
   SL_PROF_WRITE(si)
 

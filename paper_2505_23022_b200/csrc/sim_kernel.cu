@@ -612,8 +612,11 @@ __global__ void __launch_bounds__(128) sl_sim_kernel(const __grid_constant__ KAr
 // Fast kernel: running set in registers (sim_fast.cuh); hands off sims that
 // outgrow it or are flagged general-only.
 constexpr int kFastWarps = 4;
+#ifndef SL_SIM_IN_SMEM
+#define SL_SIM_IN_SMEM 1
+#endif
 #ifndef SL_HOT_MIN_BLOCKS
-#define SL_HOT_MIN_BLOCKS 3  // 12 warps/SM for the hot kernel (<= 168 registers)
+#define SL_HOT_MIN_BLOCKS 4  // 16 warps/SM for the hot kernel (<= 128 registers)
 #endif
 __device__ __forceinline__ bool hot_eligible(const sl_sim& sp) {
   const int f = SL_FLAG_TTFT_GUARD | SL_FLAG_TPOT_GUARD;
@@ -643,10 +646,21 @@ __global__ void __launch_bounds__(32 * kFastWarps, HOT ? SL_HOT_MIN_BLOCKS : 1) 
       if (lane == 0) a.results[si].status = SL_SIM_CAPACITY;
       continue;
     }
-    Sim s = make_sim(a, ws, si);
     if (HOT) {
+#if SL_SIM_IN_SMEM
+      // per-sim constants live in shared memory: re-read where used instead of
+      // pinning ~60 registers for the whole simulation
+      __shared__ Sim sim_sm[kFastWarps];
+      __syncwarp();
+      if (lane == 0) sim_sm[warp] = make_sim(a, ws, si);
+      __syncwarp();
+      const Sim& s = sim_sm[warp];
+#else
+      Sim s = make_sim(a, ws, si);
+#endif
       run_fast<false, true>(s, a, OUT && s.out_off >= 0, si, lane, scratch[warp]);
     } else {
+      Sim s = make_sim(a, ws, si);
       run_fast<false, false>(s, a, a.has_out && s.out_off >= 0, si, lane, scratch[warp]);
     }
   }

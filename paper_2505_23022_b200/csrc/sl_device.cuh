@@ -148,6 +148,11 @@ __device__ __forceinline__ cred_t<WIDE> shfl_cred(cred_t<WIDE> v, int src) {
 
 template <bool WIDE>
 __device__ __forceinline__ cred_t<WIDE> warp_min_cred(cred_t<WIDE> v) {
+  if constexpr (!WIDE) {  // two 32-bit warp reductions: high word, then low word among ties
+    const unsigned hi = __reduce_min_sync(SL_FULL, (unsigned)(v >> 32));
+    const unsigned lo = __reduce_min_sync(SL_FULL, (unsigned)(v >> 32) == hi ? (unsigned)v : ~0u);
+    return ((uint64_t)hi << 32) | lo;
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     cred_t<WIDE> w;
