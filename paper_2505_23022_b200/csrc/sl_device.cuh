@@ -152,20 +152,16 @@ __device__ __forceinline__ cred_t<WIDE> warp_min_cred(cred_t<WIDE> v) {
     const unsigned hi = __reduce_min_sync(SL_FULL, (unsigned)(v >> 32));
     const unsigned lo = __reduce_min_sync(SL_FULL, (unsigned)(v >> 32) == hi ? (unsigned)v : ~0u);
     return ((uint64_t)hi << 32) | lo;
-  }
+  } else {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    cred_t<WIDE> w;
-    if constexpr (WIDE) {
+    for (int o = 16; o; o >>= 1) {
       uint64_t lo = __shfl_xor_sync(SL_FULL, (uint64_t)v, o);
       uint64_t hi = __shfl_xor_sync(SL_FULL, (uint64_t)(v >> 64), o);
-      w = ((unsigned __int128)hi << 64) | lo;
-    } else {
-      w = __shfl_xor_sync(SL_FULL, v, o);
+      cred_t<WIDE> w = ((unsigned __int128)hi << 64) | lo;
+      v = w < v ? w : v;
     }
-    v = w < v ? w : v;
+    return v;
   }
-  return v;
 }
 
 // ---- work-step decision digest (oracle orc_digest_item).
