@@ -187,6 +187,12 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
 /* Number of kernels sl_run_batch launches per call (for the gpu_launches claim). */
 int sl_run_batch_launches(void);
 
+/* Self-test of the hot path's exact small-divisor division (device pointers):
+ * out[i] = a[i] / b[i], a[i] an integer in [0, 2^53), 1 <= b[i]; must equal the
+ * correctly rounded quotient (Python int / int), e.g. the L-average of
+ * costmodel.itl (simengine.py:235-237) and _admission_math (sched_scorpio.py:104). */
+int sl_selftest_div_small(const double* a, const int32_t* b, double* out, int64_t n, void* stream);
+
 /* ---- batched plan_step over independent SchedulerStates ---------------
  * (sched_scorpio.plan_step, sched_scorpio.py:210-316; config 2).  A batch is S
  * "segments", each one SchedulerState (schedtypes.py:60-64): its waiting items

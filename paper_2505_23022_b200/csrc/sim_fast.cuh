@@ -289,7 +289,7 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       bool lt = !has_min || tp < mind;
       double minp = lt ? tp : mind;
       double V = fmul_(minp, fadd_(inv, ic));
-      double L = fdiv_((double)(lens + ln), (double)(n_run + 1));
+      double L = div_small((double)(lens + ln), (int)(n_run + 1));
       double est = tpot_estimate(C, V, L, pred);
       double thr = (r_only && has_min) ? mind : minp;
       bool ok = ((pend >> lane) & 1u) && est <= thr;
@@ -558,7 +558,7 @@ __device__ __forceinline__ bool quiet_block(const Sim& s, const KArgs& a, bool h
     }
   }
   // C. durations in parallel, the clock serially
-  if (lane < jmax) dur[lane] = itl(C, my_nb, fdiv_((double)my_blen, (double)my_nb));
+  if (lane < jmax) dur[lane] = itl(C, my_nb, div_small((double)my_blen, my_nb));
   __syncwarp();
   {
     double t = now;
@@ -653,12 +653,7 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
       sl[0].rem -= 1;
     }
     g.lens += nb;
-    double L;
-    if ((nb & (nb - 1)) == 0)
-      L = fmul_((double)blen, __longlong_as_double((long long)(1023 - (__ffs(nb) - 1)) << 52));
-    else
-      L = fdiv_((double)blen, (double)nb);
-    const double end = fadd_(now, itl(C, nb, L));
+    const double end = fadd_(now, itl(C, nb, div_small((double)blen, nb)));
     if (lane == (int)(step - base)) {
       end_bits = (uint64_t)__double_as_longlong(end);
       d_nb = nb;
@@ -894,12 +889,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     const double prefill_s = ps_result(P);
     double decode_s = 0.0;
     if (nb > 0) {
-      double L;
-      if ((nb & (nb - 1)) == 0)  // exact: division by a power of two is a scaling
-        L = fmul_((double)blen, __longlong_as_double((long long)(1023 - (__ffs(nb) - 1)) << 52));
-      else
-        L = fdiv_((double)blen, (double)nb);
-      decode_s = itl(C, nb, L);
+      decode_s = itl(C, nb, div_small((double)blen, nb));
     }
     const double end = fadd_(fadd_(now, prefill_s), decode_s);
     acc.dig += acc.dig_rej;

@@ -701,6 +701,22 @@ int sl_credit_params(int64_t n, const double* tpot_slo, double slo_scale, int32_
   return SL_OK;
 }
 
+// Self-test hook for the exact small-divisor division used on the hot path
+// (div_small, sl_device.cuh): out[i] = a[i] / b[i] correctly rounded.
+__global__ void div_small_test_kernel(const double* a, const int32_t* b, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = div_small(a[i], b[i]);
+}
+
+int sl_selftest_div_small(const double* a, const int32_t* b, double* out, int64_t n,
+                          void* stream) {
+  if (n < 0 || (n > 0 && (!a || !b || !out))) return SL_ERR_ARG;
+  if (n == 0) return SL_OK;
+  div_small_test_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(a, b, out, n);
+  return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+}
+
 int sl_run_batch_launches(void) { return 3; }  // hot fast + generic fast + general handoff
 
 #ifdef SL_PHASE_PROF

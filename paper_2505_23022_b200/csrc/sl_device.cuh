@@ -75,6 +75,23 @@ __device__ __forceinline__ double ps_result(const PySum& s) {
   return f;
 }
 
+// ---- exact small-divisor division.  kRecip[b] = RN(1/b).  For an integer
+// 0 <= a < 2^53 and 1 <= b <= 128: q0 = RN(a*y) is within 2 ulp of a/b, so the
+// remainder r = a - b*q0 is a multiple of ulp(q0) below 2^8 ulp(q0) and the FMA
+// computes it exactly; q1 = RN(q0 + r*y) = RN(a/b + (a/b - q0)*eps), |eps| <=
+// 2^-53, and a/b is either dyadic (exact) or at least ulp/(2b) away from every
+// rounding midpoint, which that perturbation cannot cross: q1 == a / b correctly
+// rounded, i.e. Python's int / int.  Three fp64 ops instead of __ddiv_rn.
+__constant__ double kRecip[129] = {0.0, 1.0, 0.5, 0.3333333333333333, 0.25, 0.2, 0.16666666666666666, 0.14285714285714285, 0.125, 0.1111111111111111, 0.1, 0.09090909090909091, 0.08333333333333333, 0.07692307692307693, 0.07142857142857142, 0.06666666666666667, 0.0625, 0.058823529411764705, 0.05555555555555555, 0.05263157894736842, 0.05, 0.047619047619047616, 0.045454545454545456, 0.043478260869565216, 0.041666666666666664, 0.04, 0.038461538461538464, 0.037037037037037035, 0.03571428571428571, 0.034482758620689655, 0.03333333333333333, 0.03225806451612903, 0.03125, 0.030303030303030304, 0.029411764705882353, 0.02857142857142857, 0.027777777777777776, 0.02702702702702703, 0.02631578947368421, 0.02564102564102564, 0.025, 0.024390243902439025, 0.023809523809523808, 0.023255813953488372, 0.022727272727272728, 0.022222222222222223, 0.021739130434782608, 0.02127659574468085, 0.020833333333333332, 0.02040816326530612, 0.02, 0.0196078431372549, 0.019230769230769232, 0.018867924528301886, 0.018518518518518517, 0.01818181818181818, 0.017857142857142856, 0.017543859649122806, 0.017241379310344827, 0.01694915254237288, 0.016666666666666666, 0.01639344262295082, 0.016129032258064516, 0.015873015873015872, 0.015625, 0.015384615384615385, 0.015151515151515152, 0.014925373134328358, 0.014705882352941176, 0.014492753623188406, 0.014285714285714285, 0.014084507042253521, 0.013888888888888888, 0.0136986301369863, 0.013513513513513514, 0.013333333333333334, 0.013157894736842105, 0.012987012987012988, 0.01282051282051282, 0.012658227848101266, 0.0125, 0.012345679012345678, 0.012195121951219513, 0.012048192771084338, 0.011904761904761904, 0.011764705882352941, 0.011627906976744186, 0.011494252873563218, 0.011363636363636364, 0.011235955056179775, 0.011111111111111112, 0.01098901098901099, 0.010869565217391304, 0.010752688172043012, 0.010638297872340425, 0.010526315789473684, 0.010416666666666666, 0.010309278350515464, 0.01020408163265306, 0.010101010101010102, 0.01, 0.009900990099009901, 0.00980392156862745, 0.009708737864077669, 0.009615384615384616, 0.009523809523809525, 0.009433962264150943, 0.009345794392523364, 0.009259259259259259, 0.009174311926605505, 0.00909090909090909, 0.009009009009009009, 0.008928571428571428, 0.008849557522123894, 0.008771929824561403, 0.008695652173913044, 0.008620689655172414, 0.008547008547008548, 0.00847457627118644, 0.008403361344537815, 0.008333333333333333, 0.008264462809917356, 0.00819672131147541, 0.008130081300813009, 0.008064516129032258, 0.008, 0.007936507936507936, 0.007874015748031496, 0.0078125};
+
+__device__ __forceinline__ double div_small(double a, int b) {
+  if (b > 128) return fdiv_(a, (double)b);
+  const double y = kRecip[b];
+  const double q0 = fmul_(a, y);
+  const double r = __fma_rn(-q0, (double)b, a);
+  return __fma_rn(r, y, q0);
+}
+
 // ---- cost models (costmodel.py:96-138)
 __device__ __forceinline__ double prefill_time(const sl_cost& c, int32_t prompt) {
   double p = (double)prompt;  // exact (|prompt| < 2^53); int<=float compare is exact
