@@ -121,6 +121,29 @@ __device__ __forceinline__ cred_t<WIDE> running_min(const Slot<WIDE> (&sl)[kSlot
   return warp_min_cred<WIDE>(m);
 }
 
+// Time up to which the walk provably rejects nothing: item j passed at `now`
+// with prefix bound U (est0 = fl(fl(fl(now - arr) + U) + pf) <= ttft).  Until
+// the next insertion its prefix can only shrink, so at a later now1 its est stays
+// <= ttft while now1 - now < sigma - m, sigma = fl(ttft - est0),
+// m = 2^-39 (now + U + pf + sigma) >> the <= 8u relative rounding error of the
+// three-op chain at now and now1 (+ that of sigma and of this sum).  Clamped
+// to >= 0 so that the bit patterns order like the values (warp_min_nonneg).
+__device__ __forceinline__ double walk_pass_until(double now, double U, double pf, double tt,
+                                                  double est0) {
+  const double sig = fsub_(tt, est0);
+  const double m = fmul_(1.8189894035458565e-12, fadd_(fadd_(fadd_(now, U), pf), sig));
+  const double t = fsub_(fadd_(now, sig), m);
+  return t >= 0.0 ? t : 0.0;  // also maps NaN to 0 (no skipping)
+}
+
+// Warp minimum of non-negative doubles (their bit patterns order like the values).
+__device__ __forceinline__ double warp_min_nonneg(double v) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const unsigned hi = __reduce_min_sync(SL_FULL, (unsigned)(b >> 32));
+  const unsigned lo = __reduce_min_sync(SL_FULL, (unsigned)(b >> 32) == hi ? (unsigned)b : ~0u);
+  return __longlong_as_double((long long)(((uint64_t)hi << 32) | lo));
+}
+
 // TTFT prefix walk over wl[0, W) in list order (ttft_guard sched_scorpio.py:196-205;
 // early_reject sched_baselines.py:95-103).
 //  1. Certified pass: an upper bound U_j of the sequential prefix (warp scan in
@@ -131,12 +154,17 @@ __device__ __forceinline__ cred_t<WIDE> running_min(const Slot<WIDE> (&sl)[kSlot
 //  2. Otherwise the exact walk, speculative-parallel: the sequential chain
 //     assuming all undecided items are kept, lane-parallel tests, ballot for the
 //     first rejection, restart after it.
+// `until` receives the time before which the walk over the remaining queue
+// provably rejects nothing (walk_pass_until), valid until the next insertion.
 __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W,
                                           int& nrej, double now, int64_t step, Acc& acc, int lane,
-                                          int64_t lg_rej, int64_t cap_rej, double* bc) {
+                                          int64_t lg_rej, int64_t cap_rej, double* bc,
+                                          double& until) {
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   if (W < (1 << 20)) {
     const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
     double U = 0.0;
+    double tmin = kInf;
     bool all_ok = true;
     for (int c0 = 0; c0 < W && all_ok; c0 += 32) {
       const int j = c0 + lane;
@@ -157,13 +185,19 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
       double excl = __shfl_up_sync(SL_FULL, v, 1);
       if (lane == 0) excl = 0.0;
       const double Uj = fmul_(fadd_(U, excl), inflate);
-      all_ok = __all_sync(SL_FULL, !valid || fadd_(fadd_(e, Uj), pf) <= tt);
+      const double est0 = fadd_(fadd_(e, Uj), pf);
+      all_ok = __all_sync(SL_FULL, !valid || est0 <= tt);
+      if (valid) tmin = fmin(tmin, walk_pass_until(now, Uj, pf, tt, est0));
       U = fmul_(fadd_(U, __shfl_sync(SL_FULL, v, 31)), inflate);
     }
-    if (all_ok) return;
+    if (all_ok) {
+      until = warp_min_nonneg(tmin);
+      return;
+    }
   }
   double* pre = bc + 32;
   double prefix = 0.0;
+  double tmin = kInf;
   int kept = 0;
   for (int c0 = 0; c0 < W; c0 += 32) {
     const int j = c0 + lane;
@@ -205,6 +239,10 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     }
     const bool r_ = valid && ((rejm >> lane) & 1u);
     const bool keep = valid && !r_;
+    if (keep) {
+      const double mine = pre[lane];
+      tmin = fmin(tmin, walk_pass_until(now, mine, pf, tt, fadd_(fadd_(e, mine), pf)));
+    }
     const unsigned km = __ballot_sync(SL_FULL, keep);
     __syncwarp();
     if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
@@ -221,6 +259,7 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     nrej += __popc(rejm);
   }
   W = kept;
+  until = warp_min_nonneg(tmin);
 }
 
 // Position of the n-th (1-based) set bit of x; requires 1 <= n <= popc(x).
@@ -592,8 +631,12 @@ __device__ __forceinline__ bool quiet_block(const Sim& s, const KArgs& a, bool h
   return __any_sync(SL_FULL, live && sl[0].rem <= 0);  // retirement due at `now`, step - 1
 }
 
-// Quiet steps (nothing waiting, <= 32 running, credit batching, no log): the
-// general step restricted to that case.  Where at least SL_QUIET_BLOCK_MIN steps
+// Quiet steps (<= 32 running, credit batching, no log, and either nothing
+// waiting or a waiting queue that provably stays untouched: `blocked` -- the
+// admission scan fails for every request, see run_fast -- and the walk passes
+// every request while now < walk_until): the general step restricted to that
+// case, where a step's only decisions are the credit batch and the clock.
+// Where at least SL_QUIET_BLOCK_MIN steps
 // can start before the next arrival (bound below) it runs lookahead blocks
 // (quiet_block), otherwise one step per iteration, whose digest items are
 // deferred and hashed lane-parallel, 32 steps per pass (lane j keeps step base+j).
@@ -602,10 +645,11 @@ __device__ __forceinline__ bool quiet_block(const Sim& s, const KArgs& a, bool h
 // the hot instruction footprint small.
 template <bool WIDE>
 __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool has_out,
-                                            Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
-                                            double& now, int64_t& step, int64_t& n_plans,
-                                            int64_t& req_steps, double next_t, bool has_h,
-                                            Acc& acc, int lane, Slot<WIDE>* scr) {
+                                            Slot<WIDE> (&sl)[kSlots], int& R, const int W,
+                                            Agg<WIDE>& g, double& now, int64_t& step,
+                                            int64_t& n_plans, int64_t& req_steps, double next_t,
+                                            double walk_until, bool has_h, Acc& acc, int lane,
+                                            Slot<WIDE>* scr) {
   const sl_cost& C = s.cost;
   const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
   // itl is monotone in B and L for non-negative coefficients: every step then
@@ -618,8 +662,8 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   bool recheck = true;
   int jcap = 0;
   uint32_t hh = sl[0].hid;
-  while (R > 0 && R <= 32 && next_t > now && now < horizon) {
-    if (SL_QUIET_BLOCK_MIN <= 32 && recheck && mono_itl) {
+  while (R > 0 && R <= 32 && next_t > now && now < horizon && now < walk_until) {
+    if (SL_QUIET_BLOCK_MIN <= 32 && W == 0 && recheck && mono_itl) {
       recheck = false;
       const unsigned mlen = __reduce_min_sync(SL_FULL, lane < R ? (unsigned)sl[0].cur_len : ~0u);
       const double span = fsub_(fmin(next_t, horizon), now);
@@ -639,7 +683,7 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
       continue;
     }
     ++n_plans;
-    req_steps += R;
+    req_steps += R + W;
     const bool live = lane < R;
     const cred_t<WIDE> N = sl[0].N + g.Smin;
     const bool b = live && N >= sl[0].S;
@@ -730,6 +774,8 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
   int64_t step = 0, n_plans = 0, n_idle = 0, req_steps = 0;
   int status = SL_SIM_OK;
   bool blocked = false;
+  // the walk provably rejects nothing while now < walk_until (until an insertion)
+  double walk_until = ttft_guard ? -kInf : kInf;
   const bool mono = C.alpha >= 0.0 && C.gamma >= 0.0 && C.epsilon >= 0.0;  // est monotone in L
   SL_PROF_DECL
 
@@ -737,15 +783,18 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     if (next < n && next_t <= now) {
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
       blocked = false;
+      if (ttft_guard) walk_until = -kInf;  // an insertion can grow later items' prefixes
     }
     SL_PROF_MARK(0)
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
     bool ret;  // entries retire at the end of step `step - 1` (at `now`)
-    if (W == 0 && credit && !logging && R > 0 && R <= 32) {
+    // quiet / blocked steps: nothing can be admitted or rejected (W == 0, or
+    // the admission scan provably fails and the walk provably passes)
+    if (credit && !logging && R > 0 && R <= 32 && (W == 0 || (blocked && now < walk_until))) {
       SL_PROF_COUNT(9, 1)
       SL_PROF_COUNT(10, -step)
-      ret = quiet_steps<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t,
-                              has_h, acc, lane, scr);
+      ret = quiet_steps<WIDE>(s, a, has_out, sl, R, W, g, now, step, n_plans, req_steps, next_t,
+                              W > 0 ? walk_until : kInf, has_h, acc, lane, scr);
       SL_PROF_COUNT(10, step)
       SL_PROF_MARK(1)
     } else {
@@ -773,7 +822,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       if (scorpio) {
         if (ttft_guard)
           spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
-                    reinterpret_cast<double*>(scr));
+                    reinterpret_cast<double*>(scr), walk_until);
         SL_PROF_MARK(2)
         if (tpot_guard) {
           // `blocked`: every waiting request failed the admission test at a
@@ -797,7 +846,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       } else {
         if (s.policy == SL_POLICY_EARLY_REJECT)
           spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
-                    reinterpret_cast<double*>(scr));
+                    reinterpret_cast<double*>(scr), walk_until);
         int room = s.cap - R;
         int take = room > 0 ? min(room, W) : 0;
         if (take > 0)

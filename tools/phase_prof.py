@@ -35,7 +35,10 @@ cnt = out[:, 8:].sum(axis=0)
 print("counts:", dict(zip(names[8:], cnt.tolist())), "sim steps", int(res["n_steps"].sum()),
       "request_steps", int(res["request_steps"].sum()))
 print("quiet: %.1f cyc/quiet-step, %.2f steps/block" % (tot[1] / max(1, cnt[2]), cnt[2] / max(1, cnt[1])))
-i = int(np.argmax(cyc.sum(axis=1)))
+tot_s = cyc.sum(axis=1)
+order = np.argsort(-tot_s)
+print("top-8 sims by cycles (ms at 1.965 GHz):", [(int(k), round(tot_s[k] / 1.965e6, 1), int(res["n_steps"][k])) for k in order[:8]])
+i = int(order[0])
 print(f"longest sim {i}: {cyc[i].sum():.3e} cycles, steps {int(res['n_steps'][i])}")
 for k in range(8):
     print(f"  {names[k]:14s} {100 * cyc[i, k] / cyc[i].sum():5.1f}%")
