@@ -620,9 +620,8 @@ __device__ __forceinline__ bool quiet_block(const Sim& s, const KArgs& a, bool h
     sl[0].cur_len += c;
     sl[0].rem -= c;
   }
-  g.lens += __reduce_add_sync(SL_FULL, (unsigned)c);
   n_plans += K;
-  req_steps += (int64_t)K * R;
+  req_steps += (int64_t)K * R;  // (g.lens is settled by the caller)
   if (lane < K)
     acc.dig += digest_item((uint64_t)(step + lane), 2, (uint32_t)my_nb, my_bh) +
                digest_item((uint64_t)(step + lane), 3, 0, (uint64_t)__double_as_longlong(my_end));
@@ -652,74 +651,82 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
                                             Slot<WIDE>* scr) {
   const sl_cost& C = s.cost;
   const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
+  // a step runs while now < lim (next arrival, horizon, walk bound: all strict)
+  const double lim = fmin(fmin(next_t, horizon), walk_until);
   // itl is monotone in B and L for non-negative coefficients: every step then
   // lasts >= itl(1, min current length), bounding the steps before `stop`
   const bool mono_itl = C.alpha >= 0.0 && C.beta >= 0.0 && C.gamma >= 0.0 && C.delta > 0.0;
-  int64_t base = step;
+  const bool live = lane < R;
+  const uint32_t hh = sl[0].hid;
+  // per-call bookkeeping: the running set and the queue are fixed within the
+  // loop, so plan / request-step / length counters are settled at exit
+  const int64_t step0 = step;
+  const unsigned cl0 = live ? (unsigned)sl[0].cur_len : 0u;
+  int k = 0;  // steps done in this call; digest window = steps [k & ~31, k)
   uint64_t end_bits = 0;
   uint32_t d_nb = 0, d_bh = 0;
   bool have = false;
   bool recheck = true;
   int jcap = 0;
-  uint32_t hh = sl[0].hid;
-  while (R > 0 && R <= 32 && next_t > now && now < horizon && now < walk_until) {
+  bool ret = false;
+  while (R > 0 && R <= 32 && now < lim) {
     if (SL_QUIET_BLOCK_MIN <= 32 && W == 0 && recheck && mono_itl) {
       recheck = false;
-      const unsigned mlen = __reduce_min_sync(SL_FULL, lane < R ? (unsigned)sl[0].cur_len : ~0u);
+      const unsigned mlen = __reduce_min_sync(SL_FULL, live ? (unsigned)sl[0].cur_len : ~0u);
       const double span = fsub_(fmin(next_t, horizon), now);
       const double dmin = itl(C, 1, (double)mlen);
       jcap = span < 31.0 * dmin ? 1 + (int)(span / dmin) : 32;
     }
     if (jcap >= SL_QUIET_BLOCK_MIN && R <= SL_QUIET_BLOCK_RMAX) {
       if (have)
-        acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
-                   digest_item((uint64_t)(base + lane), 3, 0, end_bits);
+        acc.dig += digest_item((uint64_t)(step0 + (k & ~31) + lane), 2, d_nb, d_bh) +
+                   digest_item((uint64_t)(step0 + (k & ~31) + lane), 3, 0, end_bits);
       have = false;
-      if (quiet_block<WIDE>(s, a, has_out, sl, R, g, now, step, n_plans, req_steps, next_t,
-                            horizon, jcap, acc, lane, scr))
-        return true;
-      base = step;
+      step = step0 + k;
+      int64_t np = 0, rs = 0;
+      ret = quiet_block<WIDE>(s, a, has_out, sl, R, g, now, step, np, rs, next_t, horizon, jcap,
+                              acc, lane, scr);
+      k = (int)(step - step0);
       recheck = true;
+      if (ret) break;
       continue;
     }
-    ++n_plans;
-    req_steps += R + W;
-    const bool live = lane < R;
     const cred_t<WIDE> N = sl[0].N + g.Smin;
     const bool b = live && N >= sl[0].S;
     if (live) sl[0].N = b ? N - sl[0].S : N;
-    const unsigned bm = __ballot_sync(SL_FULL, b);
-    const int nb = __popc(bm);
+    const int nb = __popc(__ballot_sync(SL_FULL, b));
     const unsigned blen = __reduce_add_sync(SL_FULL, b ? (unsigned)sl[0].cur_len : 0u);
     const unsigned bh = __reduce_add_sync(SL_FULL, b ? hh : 0u);
     if (b) {
       sl[0].cur_len += 1;
       sl[0].rem -= 1;
     }
-    g.lens += nb;
     const double end = fadd_(now, itl(C, nb, div_small((double)blen, nb)));
-    if (lane == (int)(step - base)) {
+    if (lane == (k & 31)) {
       end_bits = (uint64_t)__double_as_longlong(end);
       d_nb = nb;
       d_bh = bh;
       have = true;
     }
-    const bool ret = __any_sync(SL_FULL, live && sl[0].rem <= 0);
+    ret = __any_sync(SL_FULL, live && sl[0].rem <= 0);
     now = end;
-    ++step;
+    ++k;
     if (ret) break;
-    if (step - base == 32) {
+    if ((k & 31) == 0) {
       if (have)
-        acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
-                   digest_item((uint64_t)(base + lane), 3, 0, end_bits);
+        acc.dig += digest_item((uint64_t)(step0 + k - 32 + lane), 2, d_nb, d_bh) +
+                   digest_item((uint64_t)(step0 + k - 32 + lane), 3, 0, end_bits);
       have = false;
-      base = step;
     }
   }
   if (have)
-    acc.dig += digest_item((uint64_t)(base + lane), 2, d_nb, d_bh) +
-               digest_item((uint64_t)(base + lane), 3, 0, end_bits);
-  return R > 0 && __any_sync(SL_FULL, lane < R && sl[0].rem <= 0);
+    acc.dig += digest_item((uint64_t)(step0 + ((k - 1) & ~31) + lane), 2, d_nb, d_bh) +
+               digest_item((uint64_t)(step0 + ((k - 1) & ~31) + lane), 3, 0, end_bits);
+  step = step0 + k;
+  n_plans += k;
+  req_steps += (int64_t)k * (R + W);
+  g.lens += __reduce_add_sync(SL_FULL, (live ? (unsigned)sl[0].cur_len : 0u) - cl0);
+  return ret;
 }
 
 // HOT: compile-time specialisation for the sweep's common case -- scorpio with
