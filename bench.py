@@ -114,37 +114,40 @@ def sample_cells(grid, n_sample: int) -> list[tuple[int, int]]:
 
 
 def cpu_reference(grid, n_sample: int, budget_s: float, threads: int):
-    """Time the C restatement (oracle/) on all host threads over a bounded sample.
+    """Time the C restatement (oracle/) on all host threads over a sample of the
+    grid's cells (stratified rate x scale; every cell when n_sample >= cells),
+    scheduled longest-first on a thread pool (ctypes drops the GIL per sim).
+    Stops submitting new cells once `budget_s` has elapsed.
 
     Returns (request_steps, seconds, n_cells, cells_desc)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import oracle as orc
 
-    pairs = sample_cells(grid, n_sample)
-    traces = {}
-    jobs = []
+    if n_sample >= grid.n_cells:
+        pairs = [(ri, si) for ri in range(len(grid.rates)) for si in range(len(grid.scales))]
+    else:
+        pairs = sample_cells(grid, n_sample)
+    pairs.sort(key=lambda p: grid.rates[p[0]])  # low rate = most steps first
     cfg = grid.config
-    for ri, si in pairs:
-        if ri not in traces:
-            traces[ri] = grid.trace_for_rate(grid.rates[ri])
-        t = traces[ri]
-        s = float(grid.scales[si])
-        jobs.append(dict(arrival=t.arrival, ttft_slo=t.ttft_slo * s, tpot_slo=t.tpot_slo * s,
-                         prompt_len=t.prompt_len, true_out=t.true_out, ids=t.id,
-                         predicted=t.predicted,
-                         params=orc.make_params(itl=cfg.itl, prefill=cfg.prefill)))
+    traces = {ri: grid.trace_for_rate(grid.rates[ri]) for ri in sorted({p[0] for p in pairs})}
+    params = orc.make_params(itl=cfg.itl, prefill=cfg.prefill)
     orc.lib()
-    rs, done = 0, 0
     t0 = time.perf_counter()
-    # run in waves of `threads` cells until the time budget is used
-    for k in range(0, len(jobs), threads):
-        out = orc.run_many(jobs[k:k + threads], threads=threads)
-        rs += sum(o["summary"]["request_steps"] for o in out)
-        done += len(out)
+
+    def one(p):
         if time.perf_counter() - t0 > budget_s:
-            break
+            return None
+        t, sc = traces[p[0]], float(grid.scales[p[1]])
+        r = orc.run_sim(t.arrival, t.ttft_slo * sc, t.tpot_slo * sc, t.prompt_len, t.true_out,
+                        t.id, t.predicted, params)
+        return r["summary"]["request_steps"]
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        out = [x for x in ex.map(one, pairs) if x is not None]
     dt = time.perf_counter() - t0
-    return rs, dt, done, f"{done} of {grid.n_cells} cells (stratified rate x scale), " \
-                         f"{grid.n_requests} requests each"
+    return sum(out), dt, len(out), f"{len(out)} of {grid.n_cells} cells " \
+                                   f"(rate x scale), {grid.n_requests} requests each"
 
 
 def run_reference_arm(args) -> None:
@@ -175,31 +178,44 @@ def run_reference_arm(args) -> None:
 
 def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
     """Config 2: one batched plan_step over 64k active requests:
-    1,024 segments x (32 waiting + 32 running), plus the 1 x (32,768 + 32,768)
-    stress segment.  The three kernels (LDF sort, guard+admission scan, credit
-    select) are timed separately with CUDA events, L2 flushed in between.
-    Algorithmic bytes per item: sort 16 B per waiting item,
-    scan 52 B per waiting + 8 B per running item, select 48 B per running item."""
+    1,024 segments x (32 waiting + 32 running), the 1 x (32,768 + 32,768) stress
+    segment, and the primary shape scaled to 4M requests (65,536 segments), where
+    the kernels are bandwidth- rather than launch/latency-bound.  The LDF sort,
+    guard+admission scan and credit select kernels are timed separately, and the
+    fused single-launch plan step (segments <= 32 waiting) as a whole; each launch
+    alone on the stream (enqueued behind a GPU sleep so no host launch overhead
+    is timed), L2 flushed before each.  Compulsory bytes (each input read once,
+    each output written once): sort 24 B read + 4 B written per waiting item;
+    scan 48 B read + 12 B written per waiting item and 12 B read per running item
+    (+ 5 x 8 B admission records for admitted items, not counted); select 25 B read
+    + 13 B written per running item; fused = the union (72 B per waiting item,
+    46 B per running item)."""
     import torch
 
     from paper_2505_23022_b200.plan import PlanBatch
-    from paper_2505_23022_b200.snapshot import config2_arrays, plan_arrays
+    from paper_2505_23022_b200.snapshot import config2_arrays, config2_plan_arrays_fast, plan_arrays
 
     itl, pre = (1e-6, 1e-3, 1e-5, 5e-3, 1.1), (0.004, 128.0, 2e-5, 1.5e-3)
     l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     out = {}
     for name, (S, W, R) in (("primary_1024x(32+32)", (1024, 32, 32)),
-                            ("stress_1x(32768+32768)", (1, 32768, 32768))):
-        pb = PlanBatch(arrays=plan_arrays(config2_arrays(S, W, R, seed=11)), device=dev)
+                            ("stress_1x(32768+32768)", (1, 32768, 32768)),
+                            ("scaled_65536x(32+32)", (65536, 32, 32))):
+        arrays = (config2_plan_arrays_fast(S, W, R, seed=11) if S > 4096 else
+                  plan_arrays(config2_arrays(S, W, R, seed=11)))
+        pb = PlanBatch(arrays=arrays, device=dev)
         Wt, Rt = S * W, S * R
         phases = {"sort": lambda: pb.sort(), "scan": lambda: pb.guard_admit(3, itl, pre),
                   "select": lambda: pb.select(3, True)}
+        if W <= 32:
+            phases["fused"] = lambda: pb.plan(3, itl, pre)
         times = {k: [] for k in phases}
         for it in range(reps + 2):
             for k, fn in phases.items():
                 l2.zero_()
                 torch.cuda.synchronize()
+                torch.cuda._sleep(200_000)  # the launch below is enqueued while this runs
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 fn()
@@ -207,15 +223,18 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
                 torch.cuda.synchronize()
                 if it >= 2:
                     times[k].append(e0.elapsed_time(e1) / 1e3)
-        bytes_ = {"sort": 16 * Wt, "scan": 52 * Wt + 8 * Rt, "select": 48 * Rt}
+        bytes_ = {"sort": 28 * Wt, "scan": 60 * Wt + 12 * Rt, "select": 38 * Rt,
+                  "fused": 72 * Wt + 46 * Rt}
         rows = {}
         for k in phases:
             t = float(np.mean(times[k]))
             rows[k] = {"us": 1e6 * t, "achieved_gbs": bytes_[k] / t / 1e9,
                        "frac": bytes_[k] / t / 1e9 / peak}
-        total = sum(float(np.mean(v)) for v in times.values())
-        out[name] = {"request_steps": Wt + Rt, "us_per_step": 1e6 * total,
-                     "request_steps_per_s": (Wt + Rt) / total, "kernels": rows}
+        sep = sum(float(np.mean(times[k])) for k in ("sort", "scan", "select"))
+        best = min(sep, float(np.mean(times["fused"]))) if "fused" in times else sep
+        out[name] = {"request_steps": Wt + Rt, "us_per_step": 1e6 * best,
+                     "request_steps_per_s": (Wt + Rt) / best, "kernels": rows}
+        del pb
     return out
 
 
@@ -370,11 +389,12 @@ def main() -> None:
     ap.add_argument("--rates", type=int, default=64)
     ap.add_argument("--scales", type=int, default=64, help="SLO scales per GPU")
     ap.add_argument("--n-requests", type=int, default=10_000)
-    ap.add_argument("--cpu-sample", type=int, default=64)
-    ap.add_argument("--cpu-budget", type=float, default=15.0,
-                    help="seconds of CPU work for the cpu_baseline sample")
-    ap.add_argument("--ref-budget", type=float, default=6.0,
-                    help="seconds of CPU work per --impl reference step")
+    ap.add_argument("--cpu-sample", type=int, default=4096,
+                    help="cells timed for cpu_baseline (>= grid size: the whole grid)")
+    ap.add_argument("--cpu-budget", type=float, default=25.0,
+                    help="wall seconds after which the cpu_baseline stops submitting cells")
+    ap.add_argument("--ref-budget", type=float, default=12.0,
+                    help="wall seconds per --impl reference step (same cell order)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-plan", action="store_true", help="skip the config-2 plan microbench")
     args = ap.parse_args()

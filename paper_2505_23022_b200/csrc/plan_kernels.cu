@@ -58,13 +58,38 @@ __device__ __forceinline__ Key inf_key() {
 }
 
 // ---- sort: one warp per segment (<= 32 items), bitonic network over shuffles
-__global__ void sort_warp_kernel(const sl_plan_state st, int32_t* perm) {
-  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (seg >= st.n_segments) return;
+__device__ __forceinline__ void seg_sort_warp(const sl_plan_state& st, int32_t* perm, int seg,
+                                              int lane) {
   const int64_t b = st.w_begin[seg];
   const int n = (int)(st.w_begin[seg + 1] - b);
   Key k = lane < n ? load_key(st, (int32_t)(b + lane)) : inf_key();
+  // Fast path: non-negative deadlines order like their bit patterns, so the
+  // network sorts packed (deadline bits, input position) pairs -- 3 shuffles per
+  // stage instead of 7.  Distinct deadlines make that the LDF order; a tie
+  // (rare) falls back to the full (deadline, arrival, id) network below.
+  if (__all_sync(SL_FULL, lane >= n || k.d >= 0.0)) {
+    uint64_t key = lane < n ? (uint64_t)__double_as_longlong(k.d) : ~0ull;
+    int32_t pos = lane;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        const uint64_t ok = __shfl_xor_sync(SL_FULL, key, j);
+        const int32_t op = __shfl_xor_sync(SL_FULL, pos, j);
+        const bool up = (lane & size) == 0;
+        const bool lower = (lane & j) == 0;
+        const bool o_lt = ok < key || (ok == key && op < pos);
+        const bool take = (lower == up) ? o_lt : !o_lt;
+        key = take ? ok : key;
+        pos = take ? op : pos;
+      }
+    }
+    const uint64_t next = __shfl_down_sync(SL_FULL, key, 1);
+    if (!__any_sync(SL_FULL, lane + 1 < n && next == key)) {
+      if (lane < n) perm[b + lane] = (int32_t)(b + pos);
+      return;
+    }
+  }
 #pragma unroll
   for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
@@ -81,6 +106,12 @@ __global__ void sort_warp_kernel(const sl_plan_state st, int32_t* perm) {
     }
   }
   if (lane < n) perm[b + lane] = k.idx;
+}
+
+__global__ void sort_warp_kernel(const sl_plan_state st, int32_t* perm) {
+  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (seg >= st.n_segments) return;
+  seg_sort_warp(st, perm, seg, threadIdx.x & 31);
 }
 
 // ---- sort: one CTA per (segment, tile of <= kTile items), bitonic over smem
@@ -176,11 +207,8 @@ __global__ void copy_kernel(const sl_plan_state st, const int32_t* __restrict__ 
 }
 
 // ---- guard + admission: one warp per segment
-__global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config cfg,
-                                   sl_plan_out out) {
-  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (seg >= st.n_segments) return;
+__device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const sl_plan_config& cfg,
+                                                const sl_plan_out& out, int seg, int lane) {
   const sl_cost& C = cfg.cost;
   const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -196,7 +224,40 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
   int32_t* kept_list = out.scratch + wb;
   int nrej = 0, kept = 0;
 
-  // 1. TTFT walk over the LDF order (speculative-parallel, exact), or the FCFS queue
+  // 1. TTFT walk over the LDF order (speculative-parallel, exact), or the FCFS queue.
+  // Certified pass first (as spec_walk in sim_fast.cuh): an inflated any-order
+  // prefix bound U_j >= the sequential prefix and monotone IEEE addition give
+  // est_j <= fl(fl(e_j + U_j) + pf_j); if that passes for every item nothing is
+  // rejected and the exact chain is not needed.
+  bool certified = !walk;
+  if (walk && W < (1 << 20)) {
+    const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
+    double U = 0.0;
+    bool all_ok = true;
+    for (int c0 = 0; c0 < W && all_ok; c0 += 32) {
+      const int p = c0 + lane;
+      const bool valid = p < W;
+      double e = 0.0, pf = 0.0, tt = 0.0;
+      if (valid) {
+        const int32_t idx = ttft_guard ? out.perm[wb + p] : (int32_t)(wb + p);
+        e = fsub_(now, st.w_arrival[idx]);
+        pf = st.w_prefill[idx];
+        tt = st.w_ttft[idx];
+      }
+      double v = pf;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(SL_FULL, v, o);
+        if (lane >= o) v = fadd_(v, y);
+      }
+      double excl = __shfl_up_sync(SL_FULL, v, 1);
+      if (lane == 0) excl = 0.0;
+      const double Uj = fmul_(fadd_(U, excl), inflate);
+      all_ok = __all_sync(SL_FULL, !valid || fadd_(fadd_(e, Uj), pf) <= tt);
+      U = fmul_(fadd_(U, __shfl_sync(SL_FULL, v, 31)), inflate);
+    }
+    certified = all_ok;
+  }
   {
     double prefix = 0.0;
     for (int c0 = 0; c0 < W; c0 += 32) {
@@ -212,16 +273,22 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
         tt = st.w_ttft[idx];
       }
       unsigned rejm = 0;
-      if (walk) {
+      if (!certified) {
+        // items failing at the chunk's incoming prefix fail at any later one
+        // (prefixes only grow, est is monotone in them): rejected outright,
+        // and the speculative chain runs over the remaining items only
+        rejm = __ballot_sync(SL_FULL, valid && fadd_(fadd_(e, prefix), pf) > tt);
         int start = 0;
         while (start < cnt) {
           double run = prefix, mine = 0.0;
           for (int t = start; t < cnt; ++t) {
+            if ((rejm >> t) & 1u) continue;
             const double x = bcast(pf, t);
             if (lane == t) mine = run;
             run = fadd_(run, x);
           }
-          const bool rj = lane >= start && lane < cnt && fadd_(fadd_(e, mine), pf) > tt;
+          const bool rj = lane >= start && lane < cnt && !((rejm >> lane) & 1u) &&
+                          fadd_(fadd_(e, mine), pf) > tt;
           const unsigned m = __ballot_sync(SL_FULL, rj);
           if (m == 0) {
             prefix = run;
@@ -282,7 +349,7 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
         const int j = c0 + lane;
         const double x = j < R ? fdiv_(1.0, st.r_tpot[rb + j]) : 0.0;
         const int cnt = min(32, R - c0);
-        for (int t = 0; t < cnt; ++t) ps_add(ps, bcast(x, t));
+        ps_add_warp(ps, x, cnt);
       }
       inv = ps_result(ps);
     }
@@ -385,7 +452,7 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
       double x = 0.0;
       if (j < tot) x = fdiv_(min_d, j < R ? st.r_tpot[rb + j] : st.w_tpot[adm[j - R]]);
       const int cnt = min(32, tot - c0);
-      for (int t = 0; t < cnt; ++t) ps_add(vs, bcast(x, t));
+      ps_add_warp(vs, x, cnt);
     }
     vbs = ps_result(vs);
   }
@@ -400,12 +467,18 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
   (void)pow2E;
 }
 
-// ---- credit select / decode-all: one warp per segment
-__global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_config cfg,
-                                     sl_plan_out out, int use_seg_min) {
+__global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config cfg,
+                                   sl_plan_out out) {
   const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   if (seg >= st.n_segments) return;
+  seg_guard_admit(st, cfg, out, seg, threadIdx.x & 31);
+}
+
+// ---- credit select / decode-all: one warp per segment
+__device__ __forceinline__ void seg_credit_select(const sl_plan_state& st,
+                                                  const sl_plan_config& cfg,
+                                                  const sl_plan_out& out, int use_seg_min,
+                                                  int seg, int lane) {
   const bool credit = cfg.flags & SL_FLAG_TPOT_GUARD;
   const int64_t rb = st.r_begin[seg];
   const int R = (int)(st.r_begin[seg + 1] - rb);
@@ -450,6 +523,33 @@ __global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_confi
     nb += __popc(bm);
   }
   if (lane == 0) out.seg_counts[4 * seg + 3] = nb;
+}
+
+__global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_config cfg,
+                                     sl_plan_out out, int use_seg_min) {
+  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (seg >= st.n_segments) return;
+  seg_credit_select(st, cfg, out, use_seg_min, seg, threadIdx.x & 31);
+}
+
+// ---- the whole plan_step in one launch (segments of <= 32 waiting items):
+// sort, guard + admission, credit select back to back in one warp; the stages
+// hand over through the segment's own global slices (L1-resident), so inputs
+// cross HBM once and there is one launch instead of three.
+__global__ void __launch_bounds__(256) plan_fused_kernel(const sl_plan_state st,
+                                                         const sl_plan_config cfg,
+                                                         sl_plan_out out) {
+  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (seg >= st.n_segments) return;
+  const int lane = threadIdx.x & 31;
+  if (cfg.flags & SL_FLAG_TTFT_GUARD) {
+    seg_sort_warp(st, out.perm, seg, lane);
+    __syncwarp();
+  }
+  seg_guard_admit(st, cfg, out, seg, lane);
+  if (cfg.flags & SL_PLAN_GUARD_ONLY) return;
+  __syncwarp();
+  seg_credit_select(st, cfg, out, 1, seg, lane);
 }
 
 __global__ void vbs_kernel(int S, const int64_t* r_begin, const double* r_tpot,
@@ -544,6 +644,20 @@ int sl_vbs_batch(int32_t n_segments, const int64_t* r_begin, const double* r_tpo
 int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64_t max_w,
                        sl_plan_out* out, void* stream) {
   if (!st || !cfg || !out) return SL_ERR_ARG;
+  if (max_w <= 32 && st->n_segments <= 8192) {  // fused single launch (small batches:
+                                                 // at scale the three kernels overlap better)
+    if (!out->scratch || !out->w_status || !out->w_pos || !out->seg_counts ||
+        ((cfg->flags & SL_FLAG_TTFT_GUARD) && !out->perm))
+      return SL_ERR_ARG;
+    if (!(cfg->flags & SL_PLAN_GUARD_ONLY) &&
+        (!out->adm_order || !out->seg_vbs || !out->seg_min_slo || !out->seg_min_fixed ||
+         !out->r_credit_out || !out->r_batch || !out->r_pos))
+      return SL_ERR_ARG;
+    if (st->n_segments == 0) return SL_OK;
+    plan_fused_kernel<<<warps_grid(st->n_segments, 256), 256, 0, (cudaStream_t)stream>>>(*st, *cfg,
+                                                                                        *out);
+    return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+  }
   int rc;
   if (cfg->flags & SL_FLAG_TTFT_GUARD) {
     rc = sl_ttft_sort_batch(st, max_w, out, stream);

@@ -214,18 +214,21 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     }
     bc[lane] = pf;
     __syncwarp();
-    unsigned rejm = 0;
+    // items failing at the chunk's incoming prefix fail at any later one
+    // (prefixes only grow, est is monotone in them): rejected outright
+    unsigned rejm = __ballot_sync(SL_FULL, valid && fadd_(fadd_(e, prefix), pf) > tt);
     int start = 0;
     while (start < cnt) {
       // assume every undecided item is kept: exact sequential prefix chain
       double run = prefix;
       for (int t = start; t < cnt; ++t) {
         if (lane == 0) pre[t] = run;
-        run = fadd_(run, bc[t]);
+        if (!((rejm >> t) & 1u)) run = fadd_(run, bc[t]);
       }
       __syncwarp();
       const double mine = pre[lane];
-      const bool rj = lane >= start && lane < cnt && fadd_(fadd_(e, mine), pf) > tt;
+      const bool rj = lane >= start && lane < cnt && !((rejm >> lane) & 1u) &&
+                      fadd_(fadd_(e, mine), pf) > tt;
       const unsigned m = __ballot_sync(SL_FULL, rj);
       if (m == 0) {
         prefix = run;

@@ -68,6 +68,20 @@ __device__ __forceinline__ void ps_add(PySum& s, double x) {
     s.f = t;
   }
 }
+// Fold the first `cnt` lanes' values of x (lane order) into s.  The operands are
+// gathered by unrolled shuffles that do not depend on the (serial) sum chain.
+__device__ __forceinline__ void ps_add_warp(PySum& s, double x, int cnt) {
+  if (cnt == 32) {
+    double v[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) v[t] = __shfl_sync(0xffffffffu, x, t);
+#pragma unroll
+    for (int t = 0; t < 32; ++t) ps_add(s, v[t]);
+  } else {
+    for (int t = 0; t < cnt; ++t) ps_add(s, __shfl_sync(0xffffffffu, x, t));
+  }
+}
+
 __device__ __forceinline__ double ps_result(const PySum& s) {
   if (s.n == 0) return 0.0;  // int 0; every use adds it to a float
   double f = s.f;

@@ -58,6 +58,37 @@ def config2_arrays(n_segments: int, w: int, r: int, seed: int, now: float = 10.0
     return a
 
 
+def config2_plan_arrays_fast(n_segments: int, w: int, r: int, seed: int, now: float = 10.0,
+                            prefill=ACC_PREFILL) -> dict[str, np.ndarray]:
+    """Vectorised sl_plan_state SoA with config2_arrays' distributions (a different
+    random stream) for large benchmark batches; not used for parity fixtures."""
+    rng = np.random.default_rng(seed)
+    S, W, R = n_segments, n_segments * w, n_segments * r
+    ttft = np.array([t[0] for t in TIERS])
+    tpot = np.array([t[1] for t in TIERS])
+    tw = rng.integers(0, 3, W)
+    tr = rng.integers(0, 3, R)
+    prompt_w = rng.integers(20, 601, W)
+    phi, theta, ap, bp = prefill
+    out_r = rng.integers(5, 401, R)
+    tokens = 1 + np.floor(rng.random(R) * (out_r - 1)).astype(np.int64)
+    E = min(math.frexp(t)[1] for _, t in TIERS) - 53
+    smin = np.uint64(int(np.ldexp(TIERS[0][1], -E)))
+    s_e = np.ldexp(tpot[tr], -E).astype(np.uint64)
+    k = rng.integers(0, 1000, R).astype(np.uint64)
+    return {
+        "w_begin": np.arange(S + 1, dtype=np.int64) * w,
+        "r_begin": np.arange(S + 1, dtype=np.int64) * r,
+        "w_arrival": now - rng.uniform(0.0, 0.4, W), "w_ttft": ttft[tw], "w_tpot": tpot[tw],
+        "w_prefill": np.where(prompt_w <= theta, phi, ap * prompt_w + bp),
+        "w_prompt": prompt_w.astype(np.int32), "w_pred": rng.integers(5, 401, W).astype(np.int32),
+        "w_id": np.arange(W, dtype=np.int64), "r_tpot": tpot[tr],
+        "r_cur_len": (rng.integers(20, 601, R) + tokens).astype(np.int32),
+        "r_id": np.arange(W, W + R, dtype=np.int64), "r_credit": (k * smin) % s_e,
+        "now": np.full(S, now), "credit_exp": np.full(S, E, np.int32),
+    }
+
+
 def plan_arrays(a: dict) -> dict[str, np.ndarray]:
     """The sl_plan_state SoA (PlanBatch(arrays=...)) of a snapshot, no objects."""
     out = {k: a[k] for k in ("w_begin", "r_begin", "w_arrival", "w_ttft", "w_tpot", "w_prefill",
