@@ -185,11 +185,13 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
     fused single-launch plan step (segments <= 32 waiting) as a whole; each launch
     alone on the stream (enqueued behind a GPU sleep so no host launch overhead
     is timed), L2 flushed before each.  Compulsory bytes (each input read once,
-    each output written once): sort 24 B read + 4 B written per waiting item;
-    scan 48 B read + 12 B written per waiting item and 12 B read per running item
-    (+ 5 x 8 B admission records for admitted items, not counted); select 25 B read
-    + 13 B written per running item; fused = the union (72 B per waiting item,
-    46 B per running item)."""
+    each output written once): sort 24 B read (arrival, ttft, id) + 4 B written
+    (perm) per waiting item; scan 44 B read (perm, arrival, prefill, ttft, tpot,
+    prompt, predicted) + 8 B written (status, position) per waiting item and 12 B
+    read (tpot, current length) per running item (admission records of admitted
+    items not counted); select 17 B read (tpot, credit, exclude) + 13 B written
+    (credit, batch flag, position) per running item; fused = the union without the
+    perm round trip (48 + 12 B per waiting item, 21 + 13 B per running item)."""
     import torch
 
     from paper_2505_23022_b200.plan import PlanBatch
@@ -223,8 +225,8 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
                 torch.cuda.synchronize()
                 if it >= 2:
                     times[k].append(e0.elapsed_time(e1) / 1e3)
-        bytes_ = {"sort": 28 * Wt, "scan": 60 * Wt + 12 * Rt, "select": 38 * Rt,
-                  "fused": 72 * Wt + 46 * Rt}
+        bytes_ = {"sort": 28 * Wt, "scan": 52 * Wt + 12 * Rt, "select": 30 * Rt,
+                  "fused": 60 * Wt + 34 * Rt}
         rows = {}
         for k in phases:
             t = float(np.mean(times[k]))
@@ -365,7 +367,8 @@ def run_ours(args) -> None:
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": src,
                          "bytes_per_unit": BYTES_PER_REQUEST_STEP,
-                         "kernel": "sl_sim_kernel", "kernel_ms": 1e3 * t_kernel},
+                         "kernel": "sl_sim_fast_kernel<hot> (+2 empty handoff launches)",
+                         "kernel_ms": 1e3 * t_kernel},
             "cpu_baseline": cpu,
             "e2e": {"value": total_rs / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
