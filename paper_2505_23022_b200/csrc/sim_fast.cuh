@@ -26,6 +26,9 @@ constexpr int kRunCap = 32 * kSlots;
 #define SL_QUIET_BLOCK_MIN 33  // lookahead block when >= this many quiet steps may start (33: never;
                                // the block code costs more icache than it saves in a sweep)
 #endif
+#ifndef SL_QUIET_UNROLL2
+#define SL_QUIET_UNROLL2 0  // two quiet steps per loop iteration
+#endif
 #ifndef SL_QUIET_BLOCK_RMAX
 #define SL_QUIET_BLOCK_RMAX 4  // ... and at most this many running (rare retirements)
 #endif
@@ -694,6 +697,71 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
       if (ret) break;
       continue;
     }
+#if SL_QUIET_UNROLL2
+    // two steps per iteration (software pipelined: the second step's credit
+    // phase and itl() overlap the first's; it commits only if the first step
+    // retires nothing and the second still starts before `lim`)
+    if ((k & 31) != 31) {
+      const cred_t<WIDE> S = sl[0].S, M = g.Smin;
+      const cred_t<WIDE> N1 = sl[0].N + M;
+      const bool bA = live && N1 >= S;
+      const cred_t<WIDE> NA = bA ? N1 - S : N1;
+      const cred_t<WIDE> N2 = NA + M;
+      const bool bB = live && N2 >= S;
+      const int nbA = __popc(__ballot_sync(SL_FULL, bA));
+      const int nbB = __popc(__ballot_sync(SL_FULL, bB));
+      const unsigned cl = live ? (unsigned)sl[0].cur_len : 0u;
+      const unsigned blA = __reduce_add_sync(SL_FULL, bA ? cl : 0u);
+      const unsigned blB = __reduce_add_sync(SL_FULL, bB ? cl + (unsigned)bA : 0u);
+      const unsigned bhA = __reduce_add_sync(SL_FULL, bA ? hh : 0u);
+      const unsigned bhB = __reduce_add_sync(SL_FULL, bB ? hh : 0u);
+      const double dA = itl(C, nbA, div_small((double)blA, nbA));
+      const double dB = itl(C, nbB, div_small((double)blB, nbB));
+      const int remA = sl[0].rem - (int)bA;
+      const bool retA = __any_sync(SL_FULL, live && remA <= 0);
+      const double endA = fadd_(now, dA);
+      if (lane == (k & 31)) {
+        end_bits = (uint64_t)__double_as_longlong(endA);
+        d_nb = nbA;
+        d_bh = bhA;
+        have = true;
+      }
+      if (!retA && endA < lim) {
+        const double endB = fadd_(endA, dB);
+        if (lane == ((k + 1) & 31)) {
+          end_bits = (uint64_t)__double_as_longlong(endB);
+          d_nb = nbB;
+          d_bh = bhB;
+          have = true;
+        }
+        if (live) {
+          sl[0].N = bB ? N2 - S : N2;
+          sl[0].cur_len += (int)bA + (int)bB;
+          sl[0].rem = remA - (int)bB;
+        }
+        ret = __any_sync(SL_FULL, live && sl[0].rem <= 0);
+        now = endB;
+        k += 2;
+      } else {
+        if (live) {
+          sl[0].N = NA;
+          sl[0].cur_len += (int)bA;
+          sl[0].rem = remA;
+        }
+        ret = retA;
+        now = endA;
+        k += 1;
+      }
+      if (ret) break;
+      if ((k & 31) == 0) {
+        if (have)
+          acc.dig += digest_item((uint64_t)(step0 + k - 32 + lane), 2, d_nb, d_bh) +
+                     digest_item((uint64_t)(step0 + k - 32 + lane), 3, 0, end_bits);
+        have = false;
+      }
+      continue;
+    }
+#endif
     const cred_t<WIDE> N = sl[0].N + g.Smin;
     const bool b = live && N >= sl[0].S;
     if (live) sl[0].N = b ? N - sl[0].S : N;
