@@ -13,6 +13,8 @@ Reference: one cell == ``slosim.simengine.run(trace, SimConfig)``
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from dataclasses import dataclass, field
 
@@ -169,7 +171,8 @@ class BatchEngine:
     def __init__(self, traces: list[TraceArrays], cells: list[Cell] | np.ndarray,
                  outcomes: bool = False, log_cells: list[int] | None = None,
                  log_steps: int = 0, log_ids: int = 0, order: np.ndarray | None = None,
-                 device=None, mode: int = N.MODE_AUTO, log_skips: int = 0):
+                 device=None, mode: int = N.MODE_AUTO, log_skips: int = 0,
+                 lookahead_frac: float = 0.0):
         torch = N.require_cuda()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
@@ -192,14 +195,24 @@ class BatchEngine:
         self._tr = {k: up(np.concatenate([getattr(t, k) for t in traces]) if traces else
                           np.zeros(0, _TRACE_DTYPES[k])) for k in TRACE_FIELDS}
         self._tr["begin"] = up(begin)
+        if order is None:
+            order = default_order(traces, sims)
+        # the longest-expected sims bound a batch's wall time: hint the kernel to
+        # run their quiet stretches as lookahead blocks (lower latency per step,
+        # more code; reserved for the critical path so the rest keep a small
+        # instruction footprint)
+        lookahead_frac = float(os.environ.get("SL_LOOKAHEAD_FRAC", lookahead_frac))
+        n_la = int(np.ceil(lookahead_frac * len(sims))) if len(sims) else 0
+        if n_la:
+            sims = sims.copy()
+            sims["flags"][np.asarray(order[:n_la])] |= N.FLAG_LOOKAHEAD
+            self.sims_host = sims
         self._sims = up(sims.view(np.uint8))
         self.total_slots = int(sum(lens[s["trace"]] for s in sims)) if len(sims) else 0
         wsb = N.lib().sl_workspace_bytes(self.total_slots, self.n_sims)
         self._ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         self._res = torch.zeros(self.n_sims * N.RESULT_DTYPE.itemsize, dtype=torch.uint8,
                                 device=dev)
-        if order is None:
-            order = default_order(traces, sims)
         self._order = up(np.ascontiguousarray(order, np.int32))
         self.st = N.SlTraces(len(traces), 0, *[self._tr[k].data_ptr() for k in (
             "begin", "arrival", "ttft_slo", "tpot_slo", "prompt_len", "true_out", "predicted",

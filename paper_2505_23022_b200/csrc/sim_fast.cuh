@@ -23,8 +23,8 @@ namespace sl {
 constexpr int kSlots = 2;
 constexpr int kRunCap = 32 * kSlots;
 #ifndef SL_QUIET_BLOCK_MIN
-#define SL_QUIET_BLOCK_MIN 33  // lookahead block when >= this many quiet steps may start (33: never;
-                               // the block code costs more icache than it saves in a sweep)
+#define SL_QUIET_BLOCK_MIN 33  // lookahead block (SL_FLAG_LOOKAHEAD sims only) when >= this many
+                              // quiet steps may start before the next arrival (33: never)
 #endif
 #ifndef SL_QUIET_UNROLL2
 #define SL_QUIET_UNROLL2 0  // two quiet steps per loop iteration
@@ -664,6 +664,7 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   const bool mono_itl = C.alpha >= 0.0 && C.beta >= 0.0 && C.gamma >= 0.0 && C.delta > 0.0;
   const bool live = lane < R;
   const uint32_t hh = sl[0].hid;
+  const bool lookahead = (s.flags & SL_FLAG_LOOKAHEAD) != 0;
   // per-call bookkeeping: the running set and the queue are fixed within the
   // loop, so plan / request-step / length counters are settled at exit
   const int64_t step0 = step;
@@ -676,7 +677,7 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   int jcap = 0;
   bool ret = false;
   while (R > 0 && R <= 32 && now < lim) {
-    if (SL_QUIET_BLOCK_MIN <= 32 && W == 0 && recheck && mono_itl) {
+    if (SL_QUIET_BLOCK_MIN <= 32 && lookahead && W == 0 && recheck && mono_itl) {
       recheck = false;
       const unsigned mlen = __reduce_min_sync(SL_FULL, live ? (unsigned)sl[0].cur_len : ~0u);
       const double span = fsub_(fmin(next_t, horizon), now);

@@ -1,0 +1,78 @@
+"""Parity at BASELINE's full size: the bench workload itself (config 3: 64 rates x
+64 SLO scales, 10k requests per sim, one sl_run_batch launch over 4,096 sims).
+
+* every cell: size-independent invariants of simengine.run (conservation of
+  requests, compliant <= completed, violation counts <= completed, goodput ==
+  compliant / sim_end, adherence == compliant / total, no engine error, request
+  steps >= steps);
+* 48 stratified cells (every rate row, scales spread over the axis, the 2 req/s
+  critical-path cells included): every result-row field and the work-step
+  digest bit-exact against the C oracle on the same traces.
+"""
+
+import numpy as np
+import pytest
+
+from tests._golden import same_float
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("n_steps", "n_plans", "n_idle_skips", "request_steps", "completed", "compliant",
+          "rejected_ttft", "rejected_admission", "incomplete", "ttft_violations",
+          "tpot_violations")
+
+
+@pytest.fixture(scope="module")
+def config3():
+    import torch
+
+    from paper_2505_23022_b200.sweep import SweepGrid, build_local
+
+    grid = SweepGrid()  # the bench's config-3 grid
+    eng, owned, traces = build_local(grid, device=torch.device("cuda", 0))
+    eng.launch()
+    return grid, eng.results(), traces
+
+
+def test_config3_invariants_every_cell(config3):
+    grid, res, _ = config3
+    assert len(res) == 4096
+    assert ((res["status"] & 3) == 0).all()
+    n = res["total"]
+    assert (n == grid.n_requests).all()
+    assert (res["completed"] + res["rejected_ttft"] + res["rejected_admission"] +
+            res["incomplete"] == n).all()
+    assert (res["incomplete"] == 0).all()  # no horizon: every request resolves
+    assert (res["compliant"] <= res["completed"]).all()
+    assert (res["ttft_violations"] <= res["completed"]).all()
+    assert (res["tpot_violations"] <= res["completed"]).all()
+    assert (res["request_steps"] >= res["n_steps"]).all()
+    h = np.maximum(res["sim_end"], 1e-12)
+    assert np.array_equal(res["goodput"], res["compliant"] / h)
+    assert np.array_equal(res["adherence"], res["compliant"] / n)
+
+
+def test_config3_sampled_cells_match_oracle(config3):
+    from oracle import oracle as orc
+
+    grid, res, traces = config3
+    ns = len(grid.scales)
+    scale_pick = [0, 9, 21, 32, 45, 63]
+    rate_pick = list(range(0, 64, 8)) + [1, 63]
+    cells = sorted({(ri, si) for ri in rate_pick for si in scale_pick})[:48]
+    params = orc.make_params(itl=grid.config.itl, prefill=grid.config.prefill)
+    jobs = []
+    for ri, si in cells:
+        t, s = traces[ri], float(grid.scales[si])
+        jobs.append(dict(arrival=t.arrival, ttft_slo=t.ttft_slo * s, tpot_slo=t.tpot_slo * s,
+                         prompt_len=t.prompt_len, true_out=t.true_out, ids=t.id,
+                         predicted=t.predicted, params=params))
+    refs = orc.run_many(jobs)
+    for (ri, si), ref in zip(cells, refs):
+        r, sm = res[ri * ns + si], ref["summary"]
+        assert ref["rc"] == 0
+        for f in FIELDS:
+            assert r[f] == sm[f], (ri, si, f, r[f], sm[f])
+        for f in ("sim_end", "goodput", "adherence"):
+            assert same_float([r[f]], [sm[f]]), (ri, si, f)
+        assert int(r["digest"]) == sm["digest"], (ri, si)
