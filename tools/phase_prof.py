@@ -25,14 +25,18 @@ lib.sl_phase_prof_read.argtypes = [C.c_void_p, C.c_int32]
 out = np.zeros((eng.n_sims, 14), np.uint64)
 assert lib.sl_phase_prof_read(out.ctypes.data, eng.n_sims) == eng.n_sims
 names = ["arrivals+top", "quiet", "walk", "inv_sum", "admit", "decode", "tail", "retire",
-         "gen_steps", "quiet_blocks", "quiet_steps", "gen_blocked", "gen_W0", "gen_R>32"]
+         "gen_steps", "quiet_blocks", "quiet_steps", "gen_blocked", "maxW", "maxR"]
 cyc = out[:, :8].astype(np.float64)
 tot = cyc.sum(axis=0)
 print("all sims: total cycles %.3e (%d sims); per-phase share:" % (tot.sum(), eng.n_sims))
 for k in range(8):
     print(f"  {names[k]:14s} {100 * tot[k] / tot.sum():5.1f}%   {tot[k] / max(1, out[:, 8].sum()):8.1f} cyc/gen-step")
-cnt = out[:, 8:].sum(axis=0)
-print("counts:", dict(zip(names[8:], cnt.tolist())), "sim steps", int(res["n_steps"].sum()),
+cnt = out[:, 8:12].sum(axis=0)
+mw, mr = out[:, 12].astype(np.int64), out[:, 13].astype(np.int64)
+print("max waiting per sim: quantiles", np.percentile(mw, [50, 90, 99, 100]).tolist(),
+      "sims with maxW > 32:", int((mw > 32).sum()), "> 64:", int((mw > 64).sum()),
+      "| max running: quantiles", np.percentile(mr, [50, 90, 99, 100]).tolist())
+print("counts:", dict(zip(names[8:12], cnt.tolist())), "sim steps", int(res["n_steps"].sum()),
       "request_steps", int(res["request_steps"].sum()))
 print("quiet: %.1f cyc/quiet-step, %.2f steps/block" % (tot[1] / max(1, cnt[2]), cnt[2] / max(1, cnt[1])))
 tot_s = cyc.sum(axis=1)
