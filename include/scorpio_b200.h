@@ -62,8 +62,6 @@ extern "C" {
 #define SL_FLAG_HAS_HORIZON 8
 #define SL_FLAG_PREFILL_PRIORITY 16
 #define SL_FLAG_GENERAL_ONLY 32 /* host: skip the register-resident fast kernel */
-#define SL_FLAG_LOOKAHEAD 64    /* host hint (no semantic effect): a critical-path sim --
-                                   run its quiet stretches as 32-step lookahead blocks */
 
 /* ---- sl_run_batch_ex modes --------------------------------------------- */
 #define SL_MODE_AUTO 0    /* fast kernel, then the general kernel for handoffs */

@@ -35,7 +35,6 @@ POLICY = {"scorpio": 0, "greedy": 1, "sjf": 2, "early_reject": 3}
 FLAG_TTFT_GUARD, FLAG_TPOT_GUARD, FLAG_R_ONLY, FLAG_HAS_HORIZON, FLAG_PREFILL_PRIORITY = (
     1, 2, 4, 8, 16)
 FLAG_GENERAL_ONLY = 32
-FLAG_LOOKAHEAD = 64  # performance hint for critical-path sims (BatchEngine sets it)
 SIM_CAPACITY = 8
 MODE_AUTO, MODE_GENERAL = 0, 1
 

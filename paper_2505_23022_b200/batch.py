@@ -13,8 +13,6 @@ Reference: one cell == ``slosim.simengine.run(trace, SimConfig)``
 
 from __future__ import annotations
 
-import os
-
 import ctypes as C
 from dataclasses import dataclass, field
 
@@ -171,8 +169,7 @@ class BatchEngine:
     def __init__(self, traces: list[TraceArrays], cells: list[Cell] | np.ndarray,
                  outcomes: bool = False, log_cells: list[int] | None = None,
                  log_steps: int = 0, log_ids: int = 0, order: np.ndarray | None = None,
-                 device=None, mode: int = N.MODE_AUTO, log_skips: int = 0,
-                 lookahead_frac: float = 0.0):
+                 device=None, mode: int = N.MODE_AUTO, log_skips: int = 0):
         torch = N.require_cuda()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
@@ -197,16 +194,6 @@ class BatchEngine:
         self._tr["begin"] = up(begin)
         if order is None:
             order = default_order(traces, sims)
-        # the longest-expected sims bound a batch's wall time: hint the kernel to
-        # run their quiet stretches as lookahead blocks (lower latency per step,
-        # more code; reserved for the critical path so the rest keep a small
-        # instruction footprint)
-        lookahead_frac = float(os.environ.get("SL_LOOKAHEAD_FRAC", lookahead_frac))
-        n_la = int(np.ceil(lookahead_frac * len(sims))) if len(sims) else 0
-        if n_la:
-            sims = sims.copy()
-            sims["flags"][np.asarray(order[:n_la])] |= N.FLAG_LOOKAHEAD
-            self.sims_host = sims
         self._sims = up(sims.view(np.uint8))
         self.total_slots = int(sum(lens[s["trace"]] for s in sims)) if len(sims) else 0
         wsb = N.lib().sl_workspace_bytes(self.total_slots, self.n_sims)

@@ -22,10 +22,6 @@ namespace sl {
 
 constexpr int kSlots = 2;
 constexpr int kRunCap = 32 * kSlots;
-#ifndef SL_QUIET_BLOCK_MIN
-#define SL_QUIET_BLOCK_MIN 33  // lookahead block (SL_FLAG_LOOKAHEAD sims only) when >= this many
-                              // quiet steps may start before the next arrival (33: never)
-#endif
 #ifndef SL_ARR_KEEP_B
 #define SL_ARR_KEEP_B 0  // keep `blocked` across arrivals that provably fail admission (measured: slower)
 #endif
@@ -34,12 +30,6 @@ constexpr int kRunCap = 32 * kSlots;
 #endif
 #ifndef SL_WALK_SKIP
 #define SL_WALK_SKIP 1  // general steps skip the walk while now < walk_until
-#endif
-#ifndef SL_QUIET_UNROLL2
-#define SL_QUIET_UNROLL2 0  // two quiet steps per loop iteration
-#endif
-#ifndef SL_QUIET_BLOCK_RMAX
-#define SL_QUIET_BLOCK_RMAX 4  // ... and at most this many running (rare retirements)
 #endif
 
 // Optional per-phase cycle accounting (profiling builds only: -DSL_PHASE_PROF,
@@ -277,15 +267,6 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
   W = kept;
   until = warp_min_nonneg(tmin);
   p_up = fmul_(prefix, 1.0 + 9.313225746154785e-10);  // kept total, inflated by 2^-30
-}
-
-// Position of the n-th (1-based) set bit of x; requires 1 <= n <= popc(x).
-__device__ __forceinline__ unsigned nth_set_bit(unsigned x, int n) {
-  unsigned lo = 0;  // invariant: popc(x & bits [0, lo)) < n
-#pragma unroll
-  for (unsigned w = 16; w; w >>= 1)
-    if (__popc(x & ((1u << (lo + w)) - 1u)) < n) lo += w;
-  return lo;
 }
 
 // Cached running-set aggregates (sched_scorpio.py:117-124), warp-uniform.
@@ -555,107 +536,16 @@ __device__ __forceinline__ void retire(const Sim& s, const KArgs& a, bool has_ou
   }
 }
 
-// One lookahead block of quiet steps (R <= 32, nothing waiting): within it the
-// membership is fixed, so every decision is a function of integer state:
-//  A. lane e runs its entry's credit recurrence (select_batch,
-//     sched_scorpio.py:171-179) for up to 32 steps: bit j of `bits` = entry
-//     batched at step j; the first retirement (the rem-th set bit) caps the block;
-//  B. per step j: batch size, length sum and id-hash sum (ballot + redux) -> lane j;
-//  C. lane j evaluates its step's itl() (simengine.py:233-238) -- all in
-//     parallel -- and only the clock now_{j+1} = now_j + d_j, which IEEE
-//     rounding makes order dependent, stays a serial chain (one DADD per
-//     step); the block ends before the first step whose start time sees an
-//     arrival or the horizon;
-//  D. the K executed steps are committed: credits in closed form (exact mod
-//     2^w, the true value lies in [0, S)), digest items (lane j: step j),
-//     retirement.
-// The empty prefill sum is 0 and now + 0 == now; the strictest entry always
-// batches, so every step has work.
-template <bool WIDE>
-__device__ __forceinline__ bool quiet_block(const Sim& s, const KArgs& a, bool has_out,
-                                            Slot<WIDE> (&sl)[kSlots], int& R, Agg<WIDE>& g,
-                                            double& now, int64_t& step, int64_t& n_plans,
-                                            int64_t& req_steps, double next_t, double horizon,
-                                            int jcap, Acc& acc, int lane, Slot<WIDE>* scr) {
-  const sl_cost& C = s.cost;
-  double* dur = reinterpret_cast<double*>(scr);  // [32] step durations
-  double* clk = dur + 32;                         // [33] step start times + block end
-  const bool live = lane < R;
-  // A. credit recurrence
-  const cred_t<WIDE> M = g.Smin, S = sl[0].S;
-  cred_t<WIDE> N = sl[0].N;
-  unsigned bits = 0u;
-  for (int j = 0; j < jcap; ++j) {
-    N += M;
-    const bool b = N >= S;
-    N = b ? N - S : N;
-    bits |= (unsigned)b << j;
-  }
-  bits = live ? bits : 0u;
-  const unsigned rj = (live && sl[0].rem <= __popc(bits)) ? nth_set_bit(bits, sl[0].rem) : 32u;
-  const int jmax = min(jcap, (int)__reduce_min_sync(SL_FULL, rj) + 1);
-  // B. per-step batch size, length sum, id-hash sum -> lane j
-  int my_nb = 0;
-  unsigned my_blen = 0, my_bh = 0;
-  {
-    unsigned cl = live ? (unsigned)sl[0].cur_len : 0u;
-    const unsigned h = sl[0].hid;
-    for (int j = 0; j < jmax; ++j) {
-      const bool b = (bits >> j) & 1u;
-      const int nb = __popc(__ballot_sync(SL_FULL, b));
-      const unsigned bl = __reduce_add_sync(SL_FULL, b ? cl : 0u);
-      const unsigned bh = __reduce_add_sync(SL_FULL, b ? h : 0u);
-      cl += b;
-      if (lane == j) {
-        my_nb = nb;
-        my_blen = bl;
-        my_bh = bh;
-      }
-    }
-  }
-  // C. durations in parallel, the clock serially
-  if (lane < jmax) dur[lane] = itl(C, my_nb, div_small((double)my_blen, my_nb));
-  __syncwarp();
-  {
-    double t = now;
-    for (int j = 0; j < jmax; ++j) {
-      if (lane == 0) clk[j] = t;
-      t = fadd_(t, dur[j]);
-    }
-    if (lane == 0) clk[jmax] = t;
-  }
-  __syncwarp();
-  const double my_start = clk[lane];
-  const double my_end = clk[lane + 1];
-  __syncwarp();
-  const unsigned runm = __ballot_sync(SL_FULL, lane < jmax && next_t > my_start && my_start < horizon);
-  const int K = (~runm == 0u) ? 32 : __ffs(~runm) - 1;  // >= 1: step 0 is quiet
-  // D. commit steps [0, K)
-  const int c = __popc(bits & (K == 32 ? ~0u : ((1u << K) - 1u)));
-  if (live) {
-    sl[0].N = sl[0].N + (cred_t<WIDE>)K * M - (cred_t<WIDE>)c * S;
-    sl[0].cur_len += c;
-    sl[0].rem -= c;
-  }
-  n_plans += K;
-  req_steps += (int64_t)K * R;  // (g.lens is settled by the caller)
-  if (lane < K)
-    acc.dig += digest_item((uint64_t)(step + lane), 2, (uint32_t)my_nb, my_bh) +
-               digest_item((uint64_t)(step + lane), 3, 0, (uint64_t)__double_as_longlong(my_end));
-  now = __shfl_sync(SL_FULL, my_end, K - 1);
-  step += K;
-  return __any_sync(SL_FULL, live && sl[0].rem <= 0);  // retirement due at `now`, step - 1
-}
-
 // Quiet steps (<= 32 running, credit batching, no log, and either nothing
 // waiting or a waiting queue that provably stays untouched: `blocked` -- the
 // admission scan fails for every request, see run_fast -- and the walk passes
 // every request while now < walk_until): the general step restricted to that
 // case, where a step's only decisions are the credit batch and the clock.
-// Where at least SL_QUIET_BLOCK_MIN steps
-// can start before the next arrival (bound below) it runs lookahead blocks
-// (quiet_block), otherwise one step per iteration, whose digest items are
-// deferred and hashed lane-parallel, 32 steps per pass (lane j keeps step base+j).
+// One step per iteration; the digest items are deferred and hashed
+// lane-parallel, 32 steps per pass (lane j keeps step base+j).  (A 32-step
+// lookahead form -- per-lane credit recurrences, parallel itl(), serial clock --
+// cut the critical-path sim by 15-25% but its code cost the sweep 10-25% in
+// instruction-cache stalls.)
 // Returns true when entries retire at the end of the last step (at `now`, step
 // index `step - 1`): the caller runs retire() -- its one call site, which keeps
 // the hot instruction footprint small.
@@ -670,12 +560,8 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
   // a step runs while now < lim (next arrival, horizon, walk bound: all strict)
   const double lim = fmin(fmin(next_t, horizon), walk_until);
-  // itl is monotone in B and L for non-negative coefficients: every step then
-  // lasts >= itl(1, min current length), bounding the steps before `stop`
-  const bool mono_itl = C.alpha >= 0.0 && C.beta >= 0.0 && C.gamma >= 0.0 && C.delta > 0.0;
   const bool live = lane < R;
   const uint32_t hh = sl[0].hid;
-  const bool lookahead = (s.flags & SL_FLAG_LOOKAHEAD) != 0;
   // per-call bookkeeping: the running set and the queue are fixed within the
   // loop, so plan / request-step / length counters are settled at exit
   const int64_t step0 = step;
@@ -684,96 +570,8 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   uint64_t end_bits = 0;
   uint32_t d_nb = 0, d_bh = 0;
   bool have = false;
-  bool recheck = true;
-  int jcap = 0;
   bool ret = false;
   while (R > 0 && R <= 32 && now < lim) {
-    if (SL_QUIET_BLOCK_MIN <= 32 && lookahead && W == 0 && recheck && mono_itl) {
-      recheck = false;
-      const unsigned mlen = __reduce_min_sync(SL_FULL, live ? (unsigned)sl[0].cur_len : ~0u);
-      const double span = fsub_(fmin(next_t, horizon), now);
-      const double dmin = itl(C, 1, (double)mlen);
-      jcap = span < 31.0 * dmin ? 1 + (int)(span / dmin) : 32;
-    }
-    if (jcap >= SL_QUIET_BLOCK_MIN && R <= SL_QUIET_BLOCK_RMAX) {
-      if (have)
-        acc.dig += digest_item((uint64_t)(step0 + (k & ~31) + lane), 2, d_nb, d_bh) +
-                   digest_item((uint64_t)(step0 + (k & ~31) + lane), 3, 0, end_bits);
-      have = false;
-      step = step0 + k;
-      int64_t np = 0, rs = 0;
-      ret = quiet_block<WIDE>(s, a, has_out, sl, R, g, now, step, np, rs, next_t, horizon, jcap,
-                              acc, lane, scr);
-      k = (int)(step - step0);
-      recheck = true;
-      if (ret) break;
-      continue;
-    }
-#if SL_QUIET_UNROLL2
-    // two steps per iteration (software pipelined: the second step's credit
-    // phase and itl() overlap the first's; it commits only if the first step
-    // retires nothing and the second still starts before `lim`)
-    if ((k & 31) != 31) {
-      const cred_t<WIDE> S = sl[0].S, M = g.Smin;
-      const cred_t<WIDE> N1 = sl[0].N + M;
-      const bool bA = live && N1 >= S;
-      const cred_t<WIDE> NA = bA ? N1 - S : N1;
-      const cred_t<WIDE> N2 = NA + M;
-      const bool bB = live && N2 >= S;
-      const int nbA = __popc(__ballot_sync(SL_FULL, bA));
-      const int nbB = __popc(__ballot_sync(SL_FULL, bB));
-      const unsigned cl = live ? (unsigned)sl[0].cur_len : 0u;
-      const unsigned blA = __reduce_add_sync(SL_FULL, bA ? cl : 0u);
-      const unsigned blB = __reduce_add_sync(SL_FULL, bB ? cl + (unsigned)bA : 0u);
-      const unsigned bhA = __reduce_add_sync(SL_FULL, bA ? hh : 0u);
-      const unsigned bhB = __reduce_add_sync(SL_FULL, bB ? hh : 0u);
-      const double dA = itl(C, nbA, div_small((double)blA, nbA));
-      const double dB = itl(C, nbB, div_small((double)blB, nbB));
-      const int remA = sl[0].rem - (int)bA;
-      const bool retA = __any_sync(SL_FULL, live && remA <= 0);
-      const double endA = fadd_(now, dA);
-      if (lane == (k & 31)) {
-        end_bits = (uint64_t)__double_as_longlong(endA);
-        d_nb = nbA;
-        d_bh = bhA;
-        have = true;
-      }
-      if (!retA && endA < lim) {
-        const double endB = fadd_(endA, dB);
-        if (lane == ((k + 1) & 31)) {
-          end_bits = (uint64_t)__double_as_longlong(endB);
-          d_nb = nbB;
-          d_bh = bhB;
-          have = true;
-        }
-        if (live) {
-          sl[0].N = bB ? N2 - S : N2;
-          sl[0].cur_len += (int)bA + (int)bB;
-          sl[0].rem = remA - (int)bB;
-        }
-        ret = __any_sync(SL_FULL, live && sl[0].rem <= 0);
-        now = endB;
-        k += 2;
-      } else {
-        if (live) {
-          sl[0].N = NA;
-          sl[0].cur_len += (int)bA;
-          sl[0].rem = remA;
-        }
-        ret = retA;
-        now = endA;
-        k += 1;
-      }
-      if (ret) break;
-      if ((k & 31) == 0) {
-        if (have)
-          acc.dig += digest_item((uint64_t)(step0 + k - 32 + lane), 2, d_nb, d_bh) +
-                     digest_item((uint64_t)(step0 + k - 32 + lane), 3, 0, end_bits);
-        have = false;
-      }
-      continue;
-    }
-#endif
     const cred_t<WIDE> N = sl[0].N + g.Smin;
     const bool b = live && N >= sl[0].S;
     if (live) sl[0].N = b ? N - sl[0].S : N;
