@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "scorpio_b200.h"
 #include "sl_device.cuh"
@@ -207,8 +208,15 @@ __global__ void copy_kernel(const sl_plan_state st, const int32_t* __restrict__ 
 }
 
 // ---- guard + admission: one warp per segment
+// GROUP: the Neumaier folds are done lane-per-segment by the caller
+// (guard_admit_group_kernel): `inv_pre` is this segment's sum(1/slo) fold, and
+// the caller folds vbs from the returned min_d / has_min / nadm.
+template <bool GROUP = false>
 __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const sl_plan_config& cfg,
-                                                const sl_plan_out& out, int seg, int lane) {
+                                                const sl_plan_out& out, int seg, int lane,
+                                                double inv_pre = 0.0, double* min_out = nullptr,
+                                                bool* has_min_out = nullptr,
+                                                int* nadm_out = nullptr) {
   const sl_cost& C = cfg.cost;
   const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -341,8 +349,8 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   int32_t* adm = out.adm_order + wb;
 
   if (tpot_guard) {
-    double inv = 0.0;
-    if (kept > 0) {
+    double inv = inv_pre;
+    if (!GROUP && kept > 0) {
       PySum ps;
       ps_init(ps);
       for (int c0 = 0; c0 < R; c0 += 32) {
@@ -441,6 +449,17 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   }
   __syncwarp();
 
+  if (GROUP) {
+    *min_out = min_d;
+    *has_min_out = has_min;
+    *nadm_out = nadm;
+    if (lane == 0) {
+      out.seg_counts[4 * seg + 0] = nwait;
+      out.seg_counts[4 * seg + 1] = nadm;
+      out.seg_counts[4 * seg + 2] = nrej;
+    }
+    return;
+  }
   // 4. plan.min_slo / plan.vbs over running + admitted, in order (:312-315)
   double vbs = 0.0;
   if (has_min) {
@@ -472,6 +491,65 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
   const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (seg >= st.n_segments) return;
   seg_guard_admit(st, cfg, out, seg, threadIdx.x & 31);
+}
+
+// Large batches: one warp per 32 segments.  The order-dependent Neumaier folds
+// (sum(1/slo) over running, sched_scorpio.py:121; vbs over running + admitted,
+// :312-315) run lane-per-segment -- one warp instruction advances 32 folds
+// instead of 32 lanes repeating one -- and the walk / admission scan run
+// warp-per-segment in between (seg_guard_admit<true>).
+__global__ void __launch_bounds__(128) guard_admit_group_kernel(const sl_plan_state st,
+                                                                const sl_plan_config cfg,
+                                                                sl_plan_out out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int seg0 = warp * 32;
+  if (seg0 >= st.n_segments) return;
+  const int nseg = min(32, st.n_segments - seg0);
+  const int my = seg0 + lane;
+  const bool mine = lane < nseg;
+  const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
+  // fold 1: sum(1.0 / slo) over this lane's segment's running entries, in order
+  double inv = 0.0;
+  if (mine && tpot_guard) {
+    const int64_t rb = st.r_begin[my], re = st.r_begin[my + 1];
+    PySum ps;
+    ps_init(ps);
+    for (int64_t j = rb; j < re; ++j) ps_add(ps, fdiv_(1.0, st.r_tpot[j]));
+    inv = ps_result(ps);
+  }
+  double min_d = 0.0;
+  bool has_min = false;
+  int nadm = 0;
+  for (int k = 0; k < nseg; ++k) {
+    double m_k = 0.0;
+    bool h_k = false;
+    int a_k = 0;
+    seg_guard_admit<true>(st, cfg, out, seg0 + k, lane, __shfl_sync(SL_FULL, inv, k), &m_k, &h_k,
+                          &a_k);
+    if (lane == k) {
+      min_d = m_k;
+      has_min = h_k;
+      nadm = a_k;
+    }
+  }
+  __syncwarp();
+  if (!mine || (cfg.flags & SL_PLAN_GUARD_ONLY)) return;
+  // fold 2: vbs = sum(min_slo / slo) over running then admitted, in order
+  double vbs = 0.0;
+  if (has_min) {
+    const int64_t rb = st.r_begin[my], re = st.r_begin[my + 1];
+    const int32_t* adm = out.adm_order + st.w_begin[my];
+    PySum vs;
+    ps_init(vs);
+    for (int64_t j = rb; j < re; ++j) ps_add(vs, fdiv_(min_d, st.r_tpot[j]));
+    for (int q = 0; q < nadm; ++q) ps_add(vs, fdiv_(min_d, st.w_tpot[adm[q]]));
+    vbs = ps_result(vs);
+  }
+  const int E = st.credit_exp[my];
+  out.seg_vbs[my] = vbs;
+  out.seg_min_slo[my] = has_min ? min_d : __longlong_as_double(0x7ff8000000000000LL);
+  out.seg_min_fixed[my] = has_min ? slo_fixed<false>(min_d, E) : ~0ull;
 }
 
 // ---- credit select / decode-all: one warp per segment
@@ -573,6 +651,14 @@ __global__ void vbs_kernel(int S, const int64_t* r_begin, const double* r_tpot,
 
 int warps_grid(int n_warps, int threads) { return (n_warps * 32 + threads - 1) / threads; }
 
+// Segment count from which guard_admit uses the 32-segments-per-warp kernel
+// (enough groups to fill the GPU); SL_PLAN_GROUP_MIN overrides it (tests force
+// either path).  The fused single-launch plan step is used below it.
+int plan_group_min() {
+  if (const char* e = getenv("SL_PLAN_GROUP_MIN")) return atoi(e);
+  return 8192;
+}
+
 }  // namespace
 
 extern "C" {
@@ -616,6 +702,11 @@ int sl_guard_admit_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_
     return SL_ERR_ARG;
   if ((cfg->flags & SL_FLAG_TTFT_GUARD) && !out->perm) return SL_ERR_ARG;
   if (st->n_segments == 0) return SL_OK;
+  if (st->n_segments >= plan_group_min()) {
+    guard_admit_group_kernel<<<warps_grid((st->n_segments + 31) / 32, 128), 128, 0,
+                               (cudaStream_t)stream>>>(*st, *cfg, *out);
+    return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+  }
   guard_admit_kernel<<<warps_grid(st->n_segments, 128), 128, 0, (cudaStream_t)stream>>>(*st, *cfg,
                                                                                         *out);
   return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
@@ -644,8 +735,8 @@ int sl_vbs_batch(int32_t n_segments, const int64_t* r_begin, const double* r_tpo
 int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64_t max_w,
                        sl_plan_out* out, void* stream) {
   if (!st || !cfg || !out) return SL_ERR_ARG;
-  if (max_w <= 32 && st->n_segments <= 8192) {  // fused single launch (small batches:
-                                                 // at scale the three kernels overlap better)
+  if (max_w <= 32 && st->n_segments < plan_group_min()) {  // fused single launch (small
+                                                           // batches; see plan_group_min)
     if (!out->scratch || !out->w_status || !out->w_pos || !out->seg_counts ||
         ((cfg->flags & SL_FLAG_TTFT_GUARD) && !out->perm))
       return SL_ERR_ARG;
