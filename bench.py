@@ -240,6 +240,72 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
     return out
 
 
+def config4_sweep(dev, reps: int = 2) -> dict:
+    """Config 4: 16,384 sims = 128 rates (2-32 req/s) x 128 SLO scales
+    (0.5-2.0), 10k requests each, ShareGPT-shaped lengths (prompt LogNormal(4.6, 0.9),
+    output LogNormal(4.5, 0.9)), with the noisy-bucket length predictor in the loop
+    (equal_width(100, 4096), error 0.73, spread 3, seed derive_seed(0, "predictor")):
+    the batched predictor kernel (sl_predict_batch, numpy-stream exact) fills every
+    trace's predicted lengths on the device, then one sl_run_batch sweeps all cells."""
+    import torch
+
+    from paper_2505_23022_b200.batch import BatchEngine, Cell
+    from paper_2505_23022_b200.predictor import Bucketing, LengthPredictor
+    from paper_2505_23022_b200.seeds import derive_seed
+    from paper_2505_23022_b200.sweep import SweepGrid
+
+    grid = SweepGrid(rates=tuple(np.linspace(2.0, 32.0, 128)),
+                     scales=tuple(np.geomspace(0.5, 2.0, 128)), prompt=(4.6, 0.9),
+                     output=(4.5, 0.9))
+    t0 = time.perf_counter()
+    traces = [grid.trace_for_rate(q) for q in grid.rates]
+    gen_s = time.perf_counter() - t0
+    pred = LengthPredictor("noisy_bucket", Bucketing.equal_width(100, 4096), error_prob=0.73,
+                           error_spread=3, rng_seed=derive_seed(0, "predictor"))
+    ids = torch.from_numpy(np.concatenate([t.id for t in traces])).to(dev)
+    tout = torch.from_numpy(np.concatenate([t.true_out for t in traces])).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    ptimes = []
+    for it in range(reps + 1):
+        torch.cuda.synchronize()
+        torch.cuda._sleep(200_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out, _ = pred.predict_device(ids, tout, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it:
+            ptimes.append(e0.elapsed_time(e1) / 1e3)
+    predicted = out.cpu().numpy()
+    k = 0
+    for t in traces:
+        t.predicted = predicted[k: k + len(t)].copy()
+        k += len(t)
+    cells = [Cell(ri, grid.config, slo_scale=float(sc)) for ri in range(len(grid.rates))
+             for sc in grid.scales]
+    eng = BatchEngine(traces, cells, device=dev)
+    eng.launch(stream)
+    torch.cuda.synchronize()
+    res = eng.results()
+    assert ((res["status"] & 3) == 0).all(), "engine error in a config-4 sim"
+    rs = int(res["request_steps"].sum())
+    times = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.launch(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    t = float(np.mean(times))
+    return {"sims": len(cells), "n_requests": grid.n_requests, "request_steps": rs,
+            "ms_per_sweep": 1e3 * t, "request_steps_per_s": rs / t,
+            "predictor": {"requests": int(len(ids)), "us": 1e6 * float(np.mean(ptimes)),
+                          "predictions_per_s": len(ids) / float(np.mean(ptimes))},
+            "mean_goodput": float(res["goodput"].mean()), "trace_gen_s": round(gen_s, 2)}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -377,6 +443,8 @@ def run_ours(args) -> None:
         }
         if not args.no_plan and world == 1:
             line["config2_plan_step"] = plan_microbench(dev, peak)
+        if not args.no_config4 and world == 1:
+            line["config4_noisy_predictor_sweep"] = config4_sweep(dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -400,6 +468,8 @@ def main() -> None:
                     help="wall seconds per --impl reference step (same cell order)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-plan", action="store_true", help="skip the config-2 plan microbench")
+    ap.add_argument("--no-config4", action="store_true",
+                    help="skip the config-4 sweep (16k sims, noisy predictor in the loop)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
