@@ -179,8 +179,9 @@ def run_reference_arm(args) -> None:
 def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
     """Config 2: one batched plan_step over 64k active requests:
     1,024 segments x (32 waiting + 32 running), the 1 x (32,768 + 32,768) stress
-    segment, and the primary shape scaled to 4M requests (65,536 segments), where
-    the kernels are bandwidth- rather than launch/latency-bound.  The LDF sort,
+    segment, and the primary shape scaled to 4M and 16.8M requests (65,536 and
+    262,144 segments), where the kernels are bandwidth- rather than
+    launch/latency-bound.  The LDF sort,
     guard+admission scan and credit select kernels are timed separately, and the
     fused single-launch plan step (segments <= 32 waiting) as a whole; each launch
     alone on the stream (enqueued behind a GPU sleep so no host launch overhead
@@ -203,7 +204,8 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
     out = {}
     for name, (S, W, R) in (("primary_1024x(32+32)", (1024, 32, 32)),
                             ("stress_1x(32768+32768)", (1, 32768, 32768)),
-                            ("scaled_65536x(32+32)", (65536, 32, 32))):
+                            ("scaled_65536x(32+32)", (65536, 32, 32)),
+                            ("scaled_262144x(32+32)", (262144, 32, 32))):
         arrays = (config2_plan_arrays_fast(S, W, R, seed=11) if S > 4096 else
                   plan_arrays(config2_arrays(S, W, R, seed=11)))
         pb = PlanBatch(arrays=arrays, device=dev)

@@ -63,34 +63,33 @@ __device__ __forceinline__ void seg_sort_warp(const sl_plan_state& st, int32_t* 
                                               int lane) {
   const int64_t b = st.w_begin[seg];
   const int n = (int)(st.w_begin[seg + 1] - b);
-  Key k = lane < n ? load_key(st, (int32_t)(b + lane)) : inf_key();
-  // Fast path: non-negative deadlines order like their bit patterns, so the
-  // network sorts packed (deadline bits, input position) pairs -- 3 shuffles per
-  // stage instead of 7.  Distinct deadlines make that the LDF order; a tie
-  // (rare) falls back to the full (deadline, arrival, id) network below.
-  if (__all_sync(SL_FULL, lane >= n || k.d >= 0.0)) {
-    uint64_t key = lane < n ? (uint64_t)__double_as_longlong(k.d) : ~0ull;
-    int32_t pos = lane;
+  // Fast path: non-negative deadlines order like their bit patterns.  The
+  // network sorts one 64-bit key per lane -- the deadline bits with the low 5
+  // bits replaced by the lane (input position) -- one 64-bit shuffle per stage.
+  // Distinct keys in the top 59 bits make that the LDF order; otherwise (ties or
+  // near-ties, rare) the full (deadline, arrival, id) network below decides.
+  double d = 0.0;
+  if (lane < n) d = fadd_(st.w_arrival[b + lane], st.w_ttft[b + lane]);  // core.py:50-53
+  if (__all_sync(SL_FULL, lane >= n || d >= 0.0)) {
+    uint64_t key = lane < n ? (((uint64_t)__double_as_longlong(d) & ~31ull) | (uint64_t)lane)
+                            : ~0ull;
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
       for (int j = size >> 1; j > 0; j >>= 1) {
         const uint64_t ok = __shfl_xor_sync(SL_FULL, key, j);
-        const int32_t op = __shfl_xor_sync(SL_FULL, pos, j);
         const bool up = (lane & size) == 0;
         const bool lower = (lane & j) == 0;
-        const bool o_lt = ok < key || (ok == key && op < pos);
-        const bool take = (lower == up) ? o_lt : !o_lt;
-        key = take ? ok : key;
-        pos = take ? op : pos;
+        key = ((lower == up) == (ok < key)) ? ok : key;
       }
     }
     const uint64_t next = __shfl_down_sync(SL_FULL, key, 1);
-    if (!__any_sync(SL_FULL, lane + 1 < n && next == key)) {
-      if (lane < n) perm[b + lane] = (int32_t)(b + pos);
+    if (!__any_sync(SL_FULL, lane + 1 < n && (next >> 5) == (key >> 5))) {
+      if (lane < n) perm[b + lane] = (int32_t)(b + (int)(key & 31));
       return;
     }
   }
+  Key k = lane < n ? load_key(st, (int32_t)(b + lane)) : inf_key();
 #pragma unroll
   for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
