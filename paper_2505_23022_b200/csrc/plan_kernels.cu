@@ -354,7 +354,7 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
       ps_init(ps);
       for (int c0 = 0; c0 < R; c0 += 32) {
         const int j = c0 + lane;
-        const double x = j < R ? fdiv_(1.0, st.r_tpot[rb + j]) : 0.0;
+        const double x = j < R ? frcp_(st.r_tpot[rb + j]) : 0.0;
         const int cnt = min(32, R - c0);
         ps_add_warp(ps, x, cnt);
       }
@@ -370,7 +370,7 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
       if (valid) {
         idx = kept_list[p];
         tp = st.w_tpot[idx];
-        ic = fdiv_(1.0, tp);
+        ic = frcp_(tp);
         ln = st.w_prompt[idx];
         pred = st.w_pred[idx];
       }
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(128) guard_admit_group_kernel(const sl_plan_st
     const int64_t rb = st.r_begin[my], re = st.r_begin[my + 1];
     PySum ps;
     ps_init(ps);
-    for (int64_t j = rb; j < re; ++j) ps_add(ps, fdiv_(1.0, st.r_tpot[j]));
+    for (int64_t j = rb; j < re; ++j) ps_add(ps, frcp_(st.r_tpot[j]));
     inv = ps_result(ps);
   }
   double min_d = 0.0;

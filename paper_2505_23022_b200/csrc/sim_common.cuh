@@ -245,7 +245,7 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
       w.prompt = s.prompt[i];
       int32_t pred = s.predicted[i];
       w.prefill = prefill_time(C, w.prompt);
-      w.inv = fdiv_(1.0, w.tpot);
+      w.inv = frcp_(w.tpot);
       w.deadline = fadd_(w.arr, w.ttft);
       cred_t<WIDE> S = slo_fixed<WIDE>(w.tpot, s.E);
       w.S = (uint64_t)S;

@@ -105,7 +105,7 @@ __device__ __forceinline__ PySum running_inv_sum(const Sim& s, const Slot<WIDE> 
     const int cnt = min(32, R - 32 * k);
     if (cnt <= 0) break;
     // 1.0 / tpot: S * 2^E is tpot exactly, so this is the WRec's inv bit for bit
-    if (32 * k + lane < R) bc[lane] = fdiv_(1.0, fixed_to_double<WIDE>(sl[k].S, s.pow2E));
+    if (32 * k + lane < R) bc[lane] = frcp_(fixed_to_double<WIDE>(sl[k].S, s.pow2E));
     __syncwarp();
     for (int t = 0; t < cnt; ++t) ps_add(ps, bc[t]);
     __syncwarp();

@@ -23,6 +23,9 @@ __device__ __forceinline__ double fadd_(double a, double b) { return __dadd_rn(a
 __device__ __forceinline__ double fsub_(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double fmul_(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double fdiv_(double a, double b) { return __ddiv_rn(a, b); }
+// 1.0 / x, correctly rounded (== fdiv_(1.0, x)): the reciprocal intrinsic has no
+// general-division slow path.
+__device__ __forceinline__ double frcp_(double x) { return __drcp_rn(x); }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
