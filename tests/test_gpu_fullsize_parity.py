@@ -76,3 +76,53 @@ def test_config3_sampled_cells_match_oracle(config3):
         for f in ("sim_end", "goodput", "adherence"):
             assert same_float([r[f]], [sm[f]]), (ri, si, f)
         assert int(r["digest"]) == sm["digest"], (ri, si)
+
+
+def test_config4_sampled_cells_match_oracle():
+    """Config 4 at full size (16,384 ShareGPT-shaped sims with the device
+    noisy-bucket predictor in the loop -- its stream is pinned to numpy's in
+    test_predictor.py): engine invariants on every cell and 24 stratified cells
+    bit-exact vs the oracle fed the same predicted lengths."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2505_23022_b200.batch import BatchEngine, Cell
+    from paper_2505_23022_b200.predictor import Bucketing, LengthPredictor
+    from paper_2505_23022_b200.seeds import derive_seed
+    from paper_2505_23022_b200.sweep import SweepGrid
+
+    dev = torch.device("cuda", 0)
+    grid = SweepGrid(rates=tuple(np.linspace(2.0, 32.0, 128)),
+                     scales=tuple(np.geomspace(0.5, 2.0, 128)), prompt=(4.6, 0.9),
+                     output=(4.5, 0.9))
+    traces = [grid.trace_for_rate(q) for q in grid.rates]
+    pred = LengthPredictor("noisy_bucket", Bucketing.equal_width(100, 4096), error_prob=0.73,
+                           error_spread=3, rng_seed=derive_seed(0, "predictor"))
+    ids = np.concatenate([t.id for t in traces])
+    tout = np.concatenate([t.true_out for t in traces])
+    out, _ = pred.predict_device(torch.from_numpy(ids).to(dev), torch.from_numpy(tout).to(dev))
+    p = out.cpu().numpy()
+    k = 0
+    for t in traces:
+        t.predicted = p[k: k + len(t)].copy()
+        k += len(t)
+    cells = [Cell(ri, grid.config, slo_scale=float(sc)) for ri in range(128) for sc in grid.scales]
+    eng = BatchEngine(traces, cells, device=dev)
+    eng.launch()
+    res = eng.results()
+    assert ((res["status"] & 3) == 0).all()
+    assert (res["completed"] + res["rejected_ttft"] + res["rejected_admission"] +
+            res["incomplete"] == res["total"]).all()
+    params = orc.make_params(itl=grid.config.itl, prefill=grid.config.prefill)
+    pick = [(ri, si) for ri in (0, 1, 17, 45, 90, 127) for si in (0, 40, 85, 127)]
+    jobs = []
+    for ri, si in pick:
+        t, s = traces[ri], float(grid.scales[si])
+        jobs.append(dict(arrival=t.arrival, ttft_slo=t.ttft_slo * s, tpot_slo=t.tpot_slo * s,
+                         prompt_len=t.prompt_len, true_out=t.true_out, ids=t.id,
+                         predicted=t.predicted, params=params))
+    for (ri, si), ref in zip(pick, orc.run_many(jobs)):
+        r, sm = res[ri * 128 + si], ref["summary"]
+        for f in FIELDS:
+            assert r[f] == sm[f], (ri, si, f, r[f], sm[f])
+        assert same_float([r["goodput"]], [sm["goodput"]]) and int(r["digest"]) == sm["digest"]
