@@ -223,38 +223,43 @@ __device__ __forceinline__ void init_outcomes(const Sim& s, const KArgs& a, int 
   }
 }
 
-// Requests with arrival <= now become visible (simengine.py:186-188): their
-// WRec is prepared lane-parallel and they join the waiting list in queue
-// order (LDF / SJF insertion or FCFS append).
+// The WaitingItem fields of request i of a sim (arrival / rate factor, scaled
+// SLOs, prefill_time, 1/slo, deadline, fixed-point slo, solo feasibility): one
+// IEEE op each, exactly as the reference builds them (core.py:50-53,
+// costmodel.py:132-138, sched_scorpio.py:279-289).
+template <bool WIDE>
+__device__ __forceinline__ WRec make_wrec(const Sim& s, int64_t i, uint64_t* S_hi) {
+  const sl_cost& C = s.cost;
+  WRec w;
+  w.arr = s.factor == 1.0 ? s.arrival[i] : fdiv_(s.arrival[i], s.factor);
+  w.ttft = fmul_(s.ttft_b[i], s.scale);
+  w.tpot = fmul_(s.tpot_b[i], s.scale);
+  w.prompt = s.prompt[i];
+  const int32_t pred = s.predicted[i];
+  w.prefill = prefill_time(C, w.prompt);
+  w.inv = frcp_(w.tpot);
+  w.deadline = fadd_(w.arr, w.ttft);
+  const cred_t<WIDE> S = slo_fixed<WIDE>(w.tpot, s.E);
+  w.S = (uint64_t)S;
+  if constexpr (WIDE) *S_hi = (uint64_t)(S >> 64);
+  const bool solo = solo_ok(C, w.tpot, w.inv, w.prompt, pred);
+  w.pred_solo = pred | (solo ? (int32_t)0x80000000 : 0);
+  return w;
+}
+
+// Requests with arrival <= now become visible (simengine.py:186-188) and join
+// the waiting list in queue order (LDF / SJF insertion or FCFS append).  Their
+// WRec were built in advance by wrec_prepass_kernel (a bandwidth-bound pass
+// over all requests of all sims), so only the queue update stays on the
+// simulation's serial path.
 template <bool WIDE>
 __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& next, double& next_t, double now,
                                  bool sorted_ldf, bool sjf, int lane) {
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  const sl_cost& C = s.cost;
   while (next < s.n && next_t <= now) {
-    int64_t i = next + lane;
-    double ai = (i < s.n) ? (s.factor == 1.0 ? s.arrival[i] : fdiv_(s.arrival[i], s.factor)) : kInf;
-    bool c = ai <= now;
-    unsigned m = __ballot_sync(SL_FULL, c);
-    int k = __popc(m);  // arrivals are sorted: m is a lane prefix
-    if (c) {
-      WRec w;
-      w.arr = ai;
-      w.ttft = fmul_(s.ttft_b[i], s.scale);
-      w.tpot = fmul_(s.tpot_b[i], s.scale);
-      w.prompt = s.prompt[i];
-      int32_t pred = s.predicted[i];
-      w.prefill = prefill_time(C, w.prompt);
-      w.inv = frcp_(w.tpot);
-      w.deadline = fadd_(w.arr, w.ttft);
-      cred_t<WIDE> S = slo_fixed<WIDE>(w.tpot, s.E);
-      w.S = (uint64_t)S;
-      if constexpr (WIDE) s.wShi[i] = (uint64_t)(S >> 64);
-      bool solo = solo_ok(C, w.tpot, w.inv, w.prompt, pred);
-      w.pred_solo = pred | (solo ? (int32_t)0x80000000 : 0);
-      s.wr[i] = w;
-    }
-    __syncwarp();
+    const int64_t i = next + lane;
+    const bool c = i < s.n && s.wr[i].arr <= now;
+    const int k = __popc(__ballot_sync(SL_FULL, c));  // arrivals are sorted: a lane prefix
     if (sorted_ldf || sjf) {
       for (int t = 0; t < k; ++t) insert_sorted(s, W, (int)(next + t), sjf, lane);
     } else {
@@ -263,7 +268,7 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
       W += k;
     }
     next += k;
-    next_t = next < s.n ? (s.factor == 1.0 ? s.arrival[next] : fdiv_(s.arrival[next], s.factor)) : kInf;
+    next_t = next < s.n ? s.wr[next].arr : kInf;
   }
 }
 

@@ -725,7 +725,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
 
   double now = 0.0;
   int64_t next = 0;
-  double next_t = n > 0 ? fdiv_(s.arrival[0], s.factor) : kInf;
+  double next_t = n > 0 ? s.wr[0].arr : kInf;  // WRec built by wrec_prepass_kernel
   int W = 0, R = 0;
   int64_t step = 0, n_plans = 0, n_idle = 0, req_steps = 0;
   int status = SL_SIM_OK;

@@ -618,6 +618,29 @@ constexpr int kFastWarps = 4;
 #ifndef SL_HOT_MIN_BLOCKS
 #define SL_HOT_MIN_BLOCKS 4  // 16 warps/SM for the hot kernel (<= 128 registers)
 #endif
+// WRec of every request of every sim handled by the fast kernels, built ahead
+// of the simulation: one thread per (sim, request), streaming the shared trace
+// and writing 64 B per request -- HBM-bound work taken off each simulation's
+// serial step chain.  (The general kernel builds its own at arrival.)
+__global__ void __launch_bounds__(256) wrec_prepass_kernel(const __grid_constant__ KArgs a) {
+  const int si = blockIdx.y;
+  const sl_sim& sp = a.sims[si];
+  Workspace ws = carve(a.ws_base, a.slots);
+  const int t = sp.trace;
+  const int64_t n = a.tr.begin[t + 1] - a.tr.begin[t];
+  Sim s = make_sim(a, ws, si);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t hi = 0;
+    if (sp.credit_wide) {
+      s.wr[i] = make_wrec<true>(s, i, &hi);
+      s.wShi[i] = hi;
+    } else {
+      s.wr[i] = make_wrec<false>(s, i, &hi);
+    }
+  }
+}
+
 __device__ __forceinline__ bool hot_eligible(const sl_sim& sp) {
   const int f = SL_FLAG_TTFT_GUARD | SL_FLAG_TPOT_GUARD;
   return sp.policy == SL_POLICY_SCORPIO && (sp.flags & f) == f &&
@@ -717,7 +740,7 @@ int sl_selftest_div_small(const double* a, const int32_t* b, double* out, int64_
   return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
 }
 
-int sl_run_batch_launches(void) { return 3; }  // hot fast + generic fast + general handoff
+int sl_run_batch_launches(void) { return 4; }  // WRec pre-pass + hot fast + generic fast + handoff
 
 #ifdef SL_PHASE_PROF
 // Profiling builds only: per-sim phase cycles / counts of the fast kernel.
@@ -781,6 +804,11 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(workspace, 0, 256, st) != cudaSuccess) return SL_ERR_CUDA;
+  if (mode == SL_MODE_AUTO) {  // WaitingItem fields of every request, ahead of the fast kernels
+    dim3 grid(8, (unsigned)n_sims);  // 8 x 256 threads per sim, grid-stride over its requests
+    wrec_prepass_kernel<<<grid, 256, 0, st>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return SL_ERR_CUDA;
+  }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
