@@ -300,8 +300,7 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
     const bool valid = j < W;
     int idx = 0;
     double tp = 0.0, ic = 0.0, pf = 0.0;
-    int32_t ln = 0, ps_ = 0, tout = 0;
-    int64_t rid = 0;
+    int32_t ln = 0, ps_ = 0;
     cred_t<WIDE> Sc = 0;
     if (valid) {
       idx = s.wl[j];
@@ -311,8 +310,6 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       pf = w.prefill;
       ln = w.prompt;
       ps_ = w.pred_solo;
-      tout = s.true_out[idx];
-      rid = s.id[idx];
       if constexpr (WIDE)
         Sc = ((unsigned __int128)s.wShi[idx] << 64) | w.S;
       else
@@ -341,6 +338,7 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       unsigned rm = __ballot_sync(SL_FULL, rj);
       if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
       if (rj) {
+        const int64_t rid = s.id[idx];  // ids / lengths only for decided requests
         int pos = nrej + __popc(rm & lanemask_lt());
         acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u + 1u);
         acc.rej_adm++;
@@ -359,12 +357,12 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       Slot<WIDE> e;
       e.N = 0;
       e.S = shfl_cred<WIDE>(Sc, gl);
-      e.id = bcast(rid, gl);
+      e.idx = bcast(idx, gl);
+      e.id = s.id[e.idx];
       e.hid = batch_hid((uint64_t)e.id);
       const double e_inv = bcast(ic, gl);
-      e.idx = bcast(idx, gl);
       e.cur_len = bcast(ln, gl);
-      e.rem = bcast(tout, gl);
+      e.rem = s.true_out[e.idx];
       const double tp_g = bcast(tp, gl);
       const double pf_g = bcast(pf, gl);
       const bool lt_g = bcast((int)lt, gl) != 0;
