@@ -299,21 +299,15 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
     const int j = c0 + lane;
     const bool valid = j < W;
     int idx = 0;
-    double tp = 0.0, ic = 0.0, pf = 0.0;
+    double tp = 0.0, ic = 0.0;
     int32_t ln = 0, ps_ = 0;
-    cred_t<WIDE> Sc = 0;
-    if (valid) {
+    if (valid) {  // the test's inputs; prefill / fixed slo are read for the admitted only
       idx = s.wl[j];
       const WRec& w = s.wr[idx];
       tp = w.tpot;
       ic = w.inv;
-      pf = w.prefill;
       ln = w.prompt;
       ps_ = w.pred_solo;
-      if constexpr (WIDE)
-        Sc = ((unsigned __int128)s.wShi[idx] << 64) | w.S;
-      else
-        Sc = w.S;
     }
     const int32_t pred = ps_ & 0x7fffffff;
     const bool solo = (ps_ & (int32_t)0x80000000) != 0;
@@ -356,15 +350,19 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       }
       Slot<WIDE> e;
       e.N = 0;
-      e.S = shfl_cred<WIDE>(Sc, gl);
       e.idx = bcast(idx, gl);
+      const WRec& wg = s.wr[e.idx];
+      if constexpr (WIDE)
+        e.S = ((unsigned __int128)s.wShi[e.idx] << 64) | wg.S;
+      else
+        e.S = wg.S;
       e.id = s.id[e.idx];
       e.hid = batch_hid((uint64_t)e.id);
       const double e_inv = bcast(ic, gl);
       e.cur_len = bcast(ln, gl);
       e.rem = s.true_out[e.idx];
       const double tp_g = bcast(tp, gl);
-      const double pf_g = bcast(pf, gl);
+      const double pf_g = wg.prefill;
       const bool lt_g = bcast((int)lt, gl) != 0;
       put_slot<WIDE>(sl, R, e, lane);
       if (lg_adm >= 0 && a.log.adm_rec) {  // AdmissionRecord inputs (sched_scorpio.py:254-271)
