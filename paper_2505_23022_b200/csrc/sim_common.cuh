@@ -147,11 +147,16 @@ __device__ __forceinline__ void insert_sorted(const Sim& s, int& W, int idx, boo
   for (int c0 = 0; c0 < W; c0 += 32) {
     int j = c0 + lane;
     bool lt = false;
-    if (j < W) {
-      int o = s.wl[j];
+    if (j < W) {  // primary key first; arrival / id read only on a tie
+      const int o = s.wl[j];
       const WRec& r = s.wr[o];
-      lt = sjf ? key_less_sjf(s, r.pred_solo & 0x7fffffff, r.arr, o, pk, ak, idx)
-               : key_less_ldf(s, r.deadline, r.arr, o, dk, ak, idx);
+      if (sjf) {
+        const int32_t pr = r.pred_solo & 0x7fffffff;
+        lt = pr != pk ? pr < pk : key_less_sjf(s, pr, r.arr, o, pk, ak, idx);
+      } else {
+        const double dr = r.deadline;
+        lt = dr != dk ? dr < dk : key_less_ldf(s, dr, r.arr, o, dk, ak, idx);
+      }
     }
     pos += __popc(__ballot_sync(SL_FULL, lt));
   }
@@ -258,7 +263,8 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   while (next < s.n && next_t <= now) {
     const int64_t i = next + lane;
-    const bool c = i < s.n && s.wr[i].arr <= now;
+    // arrival / rate factor: the trace value itself when the factor is 1 (x / 1.0 == x)
+    const bool c = i < s.n && (s.factor == 1.0 ? s.arrival[i] : s.wr[i].arr) <= now;
     const int k = __popc(__ballot_sync(SL_FULL, c));  // arrivals are sorted: a lane prefix
     if (sorted_ldf || sjf) {
       for (int t = 0; t < k; ++t) insert_sorted(s, W, (int)(next + t), sjf, lane);
@@ -268,7 +274,7 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
       W += k;
     }
     next += k;
-    next_t = next < s.n ? s.wr[next].arr : kInf;
+    next_t = next < s.n ? (s.factor == 1.0 ? s.arrival[next] : s.wr[next].arr) : kInf;
   }
 }
 
