@@ -22,12 +22,6 @@ namespace sl {
 
 constexpr int kSlots = 2;
 constexpr int kRunCap = 32 * kSlots;
-#ifndef SL_ARR_KEEP_B
-#define SL_ARR_KEEP_B 0  // keep `blocked` across arrivals that provably fail admission (measured: slower)
-#endif
-#ifndef SL_ARR_KEEP_W
-#define SL_ARR_KEEP_W 1  // keep the walk bound across insertions (shifted by their prefill)
-#endif
 #ifndef SL_WALK_SKIP
 #define SL_WALK_SKIP 1  // general steps skip the walk while now < walk_until
 #endif
@@ -606,72 +600,47 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   return ret;
 }
 
-// New arrivals (requests [n0, n0 + kn), their WRec just written) inserted into
-// a waiting queue whose state is `blocked` (every queued request fails the
-// admission scan and is feasible alone) with a walk bound `walk_until`:
-//  * blocked survives iff every new request also fails the admission test
-//    against the current running aggregates (the state the next scan starts
-//    from) and is feasible alone -- then no scan can admit or reject anything;
-//  * an insertion grows the prefixes of later requests by at most
-//    D = (sum of new prefills) (1 + 2^-30) + 2^-30 p_up (a fresh fl-sum of
-//    n < 2^20 positive terms stays within 2^-30 of any other order), which
-//    lowers every old bound by at most D (est has slope 1 in the prefix; the
-//    rounding margin m of walk_pass_until is unchanged since sigma + U is);
-//    each new request gets its own bound with prefix <= p_up + D.
-// Otherwise the flags are cleared and the next step runs the full scan / walk.
-template <bool WIDE>
-__device__ __forceinline__ void arrivals_keep_bounds(const Sim& s, const Agg<WIDE>& g, int R,
-                                                     int W, int64_t n0, int kn, double now,
-                                                     bool r_only, bool mono, bool ttft_guard,
-                                                     bool& blocked, double& walk_until,
-                                                     double& p_up, int lane) {
+// New arrivals (requests [n0, n0 + kn), their WRec already built) inserted into
+// a waiting queue with a walk bound `walk_until`: an insertion grows the
+// prefixes of later requests by at most D = (sum of new prefills) (1 + 2^-30)
+// + 2^-30 p_up (a fresh fl-sum of n < 2^20 positive terms stays within 2^-30 of
+// any other order), which lowers every old bound by at most D (est has slope 1
+// in the prefix; the rounding margin m of walk_pass_until is unchanged since
+// sigma + U is); each new request gets its own bound with prefix <= p_up + D.
+// `blocked` is cleared: the next step runs the admission scan.  (Keeping it
+// when every new request provably fails too was measured slower.)
+__device__ __forceinline__ void arrivals_keep_bounds(const Sim& s, int64_t n0, int kn, double now,
+                                                     bool ttft_guard, bool& blocked,
+                                                     double& walk_until, double& p_up, int lane) {
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  const bool keep_b = SL_ARR_KEEP_B && blocked && mono && g.inv_valid && R > 0 && kn <= 32;
-  const bool keep_w = SL_ARR_KEEP_W && ttft_guard && walk_until > now && kn <= 32;
+  const bool keep_w = ttft_guard && walk_until > now && kn <= 32;
   const double wu_old = walk_until;
   blocked = false;
   if (ttft_guard) walk_until = -kInf;
-  if (!keep_b && !keep_w) return;
+  if (!keep_w) return;
   const bool v = lane < kn;
-  double tp = 1.0, ic = 0.0, pf = 0.0, arr = 0.0, tt = 0.0;
-  int32_t ln = 0, ps_ = 0;
+  double pf = 0.0, arr = 0.0, tt = 0.0;
   if (v) {
     const WRec& w = s.wr[n0 + lane];
-    tp = w.tpot;
-    ic = w.inv;
     pf = w.prefill;
     arr = w.arr;
     tt = w.ttft;
-    ln = w.prompt;
-    ps_ = w.pred_solo;
   }
-  if (keep_b) {  // _admission_math at the current state, as spec_admit's first round
-    const double mind = g.min_d;
-    const double minp = tp < mind ? tp : mind;
-    const double V = fmul_(minp, fadd_(ps_result(g.pinv), ic));
-    const double L = div_small((double)(g.lens + ln), R + 1);
-    const double est = tpot_estimate(s.cost, V, L, ps_ & 0x7fffffff);
-    const double thr = r_only ? mind : minp;
-    blocked = __all_sync(SL_FULL, !v || (!(est <= thr) && (ps_ & (int32_t)0x80000000) != 0));
-  }
-  if (keep_w) {
-    const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
-    double sp = pf;  // sum of the new prefills (any order; inflated below)
+  const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
+  double sp = pf;  // sum of the new prefills (any order; inflated below)
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sp = fadd_(sp, __shfl_xor_sync(SL_FULL, sp, o));
-    const double D = fadd_(fmul_(sp, inflate), fmul_(p_up, 9.313225746154785e-10));
-    const double Dup = fmul_(D, 1.0 + 1.1368683772161603e-13);  // + 2^-43: rounding of D
-    const double old_w = fsub_(fsub_(wu_old, Dup), fmul_(wu_old, 9.094947017729282e-13));
-    const double Ux = fmul_(fadd_(p_up, Dup), inflate);  // bound on a new request's prefix
-    double tx = kInf;
-    if (v) {
-      const double est0 = fadd_(fadd_(fsub_(now, arr), Ux), pf);
-      tx = est0 <= tt ? walk_pass_until(now, Ux, pf, tt, est0) : 0.0;
-    }
-    const double t_new = warp_min_nonneg(tx);
-    walk_until = fmin(old_w, t_new);
-    p_up = Ux;
+  for (int o = 16; o; o >>= 1) sp = fadd_(sp, __shfl_xor_sync(SL_FULL, sp, o));
+  const double D = fadd_(fmul_(sp, inflate), fmul_(p_up, 9.313225746154785e-10));
+  const double Dup = fmul_(D, 1.0 + 1.1368683772161603e-13);  // + 2^-43: rounding of D
+  const double old_w = fsub_(fsub_(wu_old, Dup), fmul_(wu_old, 9.094947017729282e-13));
+  const double Ux = fmul_(fadd_(p_up, Dup), inflate);  // bound on a new request's prefix
+  double tx = kInf;
+  if (v) {
+    const double est0 = fadd_(fadd_(fsub_(now, arr), Ux), pf);
+    tx = est0 <= tt ? walk_pass_until(now, Ux, pf, tt, est0) : 0.0;
   }
+  walk_until = fmin(old_w, warp_min_nonneg(tx));
+  p_up = Ux;
 }
 
 // HOT: compile-time specialisation for the sweep's common case -- scorpio with
@@ -736,8 +705,8 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
     if (next < n && next_t <= now) {
       const int64_t n0 = next;
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
-      arrivals_keep_bounds<WIDE>(s, g, R, W, n0, (int)(next - n0), now, r_only, mono, ttft_guard,
-                                 blocked, walk_until, p_up, lane);
+      arrivals_keep_bounds(s, n0, (int)(next - n0), now, ttft_guard, blocked, walk_until, p_up,
+                           lane);
     }
     SL_PROF_MARK(0)
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
