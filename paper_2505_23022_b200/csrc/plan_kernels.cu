@@ -267,17 +267,32 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   }
   {
     double prefix = 0.0;
+    // software pipelined over chunks (large segments are DRAM-latency bound):
+    // queue slots of chunk c+2 and the fields of chunk c+1 are requested before
+    // chunk c is walked
+    auto slot = [&](int c0) -> int32_t {
+      const int p = c0 + lane;
+      return p < W ? (ttft_guard ? out.perm[wb + p] : (int32_t)(wb + p)) : -1;
+    };
+    int32_t idx_n = slot(0), idx_nn = slot(32);
+    double ar_n = 0.0, pf_n = 0.0, tt_n = 0.0;
+    if (idx_n >= 0) {
+      ar_n = st.w_arrival[idx_n];
+      pf_n = st.w_prefill[idx_n];
+      tt_n = st.w_ttft[idx_n];
+    }
     for (int c0 = 0; c0 < W; c0 += 32) {
       const int p = c0 + lane;
       const bool valid = p < W;
       const int cnt = min(32, W - c0);
-      int32_t idx = 0;
-      double e = 0.0, pf = 0.0, tt = 0.0;
-      if (valid) {
-        idx = ttft_guard ? out.perm[wb + p] : (int32_t)(wb + p);
-        e = fsub_(now, st.w_arrival[idx]);
-        pf = st.w_prefill[idx];
-        tt = st.w_ttft[idx];
+      const int32_t idx = valid ? idx_n : 0;
+      const double e = fsub_(now, ar_n), pf = pf_n, tt = tt_n;
+      idx_n = idx_nn;
+      idx_nn = slot(c0 + 64);
+      if (idx_n >= 0) {
+        ar_n = st.w_arrival[idx_n];
+        pf_n = st.w_prefill[idx_n];
+        tt_n = st.w_ttft[idx_n];
       }
       unsigned rejm = 0;
       if (!certified) {
@@ -336,6 +351,7 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   // 2. running aggregates (sched_scorpio.py:117-124)
   int64_t lens = 0;
   double min_d = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll 4
   for (int j = lane; j < R; j += 32) {
     lens += st.r_cur_len[rb + j];
     min_d = fmin(min_d, st.r_tpot[rb + j]);
@@ -352,11 +368,12 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
     if (!GROUP && kept > 0) {
       PySum ps;
       ps_init(ps);
+      double t_n = lane < R ? st.r_tpot[rb + lane] : 1.0;  // next chunk's operand, in flight
       for (int c0 = 0; c0 < R; c0 += 32) {
-        const int j = c0 + lane;
-        const double x = j < R ? frcp_(st.r_tpot[rb + j]) : 0.0;
-        const int cnt = min(32, R - c0);
-        ps_add_warp(ps, x, cnt);
+        const double x = frcp_(t_n);
+        const int jn = c0 + 32 + lane;
+        t_n = jn < R ? st.r_tpot[rb + jn] : 1.0;
+        ps_add_warp(ps, x, min(32, R - c0));
       }
       inv = ps_result(ps);
     }
@@ -465,12 +482,12 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
     PySum vs;
     ps_init(vs);
     const int tot = R + nadm;
+    auto slo = [&](int j) { return j < tot ? (j < R ? st.r_tpot[rb + j] : st.w_tpot[adm[j - R]]) : 1.0; };
+    double t_n = slo(lane);  // next chunk's operand, in flight
     for (int c0 = 0; c0 < tot; c0 += 32) {
-      const int j = c0 + lane;
-      double x = 0.0;
-      if (j < tot) x = fdiv_(min_d, j < R ? st.r_tpot[rb + j] : st.w_tpot[adm[j - R]]);
-      const int cnt = min(32, tot - c0);
-      ps_add_warp(vs, x, cnt);
+      const double x = fdiv_(min_d, t_n);
+      t_n = slo(c0 + 32 + lane);
+      ps_add_warp(vs, x, min(32, tot - c0));
     }
     vbs = ps_result(vs);
   }
