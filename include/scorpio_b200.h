@@ -142,6 +142,16 @@ typedef struct {
   double* tpot;
 } sl_outcomes;
 
+/* Per-sim RunReport reductions (report.summarize, report.py:71-127) computed on
+ * the device from the outcomes an sl_run_batch wrote (cells with outcomes):
+ * nearest-rank p50/p90/p99 of TTFT (s) and TPOT (ms) over completed requests
+ * (NaN when none; n_completed = -1 for cells without outcomes). */
+typedef struct {
+  double ttft_p[3];
+  double tpot_ms_p[3];
+  int64_t n_completed;
+} sl_report_row;
+
 /* Optional decision log (EventLog.steps, simengine.py:80-137), one row per
  * sim with log_slot >= 0: step_cap steps and id_cap ids per stream per row.
  * Ids of step k are the next n_admitted[k] / n_rejected[k] / n_batch[k]
@@ -183,6 +193,14 @@ int sl_run_batch(const sl_traces* traces, const sl_sim* sims, const int32_t* ord
 int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* order,
                     int32_t n_sims, void* workspace, int64_t total_slots, sl_result* results,
                     const sl_outcomes* outcomes, const sl_log* log, int32_t mode, void* stream);
+
+/* RunReport reductions for n_sims cells (one launch): rows[n_sims]; per-category
+ * totals / compliant counts cat_counts[n_sims][n_categories][2] for categories
+ * 0..n_categories-1 (category[begin[t] + i] = category of request i of trace t,
+ * may be NULL = all 0).  Replaces the per-run summarize() loop of report.sweep. */
+int sl_report_batch(const sl_traces* traces, const sl_sim* sims, int32_t n_sims,
+                    const sl_outcomes* outcomes, const int8_t* category, int32_t n_categories,
+                    sl_report_row* rows, int64_t* cat_counts, void* stream);
 
 /* Number of kernels sl_run_batch launches per call (for the gpu_launches claim). */
 int sl_run_batch_launches(void);

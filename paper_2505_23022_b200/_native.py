@@ -19,7 +19,7 @@ LIB_DIR = os.path.join(PKG, "lib")
 LIB_PATH = os.environ.get("SL_LIB_PATH") or os.path.join(LIB_DIR, "libscorpio_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ("sim_kernel.cu", "plan_kernels.cu", "predict_kernel.cu")
+SOURCES = ("sim_kernel.cu", "plan_kernels.cu", "predict_kernel.cu", "report_kernel.cu")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -58,6 +58,15 @@ RESULT_DTYPE = np.dtype({
     "formats": ["<i4", "<i4"] + ["<i8"] * 12 + ["<f8"] * 4 + ["<u8"],
     "offsets": [0, 4] + [8 + 8 * k for k in range(12)] + [104, 112, 120, 128, 136],
     "itemsize": 144,
+})
+
+
+REPORT_DTYPE = np.dtype({  # sl_report_row
+    "names": ["ttft_p50", "ttft_p90", "ttft_p99", "tpot_ms_p50", "tpot_ms_p90", "tpot_ms_p99",
+              "n_completed"],
+    "formats": ["<f8"] * 6 + ["<i8"],
+    "offsets": [8 * k for k in range(7)],
+    "itemsize": 56,
 })
 
 
@@ -160,6 +169,10 @@ def lib():
                                   C.POINTER(SlLog), C.c_int32, C.c_void_p]
     L.sl_run_batch_ex.restype = C.c_int
     L.sl_run_batch_launches.restype = C.c_int
+    L.sl_report_batch.argtypes = [C.POINTER(SlTraces), C.c_void_p, C.c_int32,
+                                  C.POINTER(SlOutcomes), C.c_void_p, C.c_int32, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]
+    L.sl_report_batch.restype = C.c_int
     L.sl_selftest_div_small.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     L.sl_selftest_div_small.restype = C.c_int
     L.sl_abi_layout.argtypes = [C.POINTER(C.c_int64), C.c_int32]

@@ -266,6 +266,36 @@ class BatchEngine:
     def results_device(self):
         return self._res
 
+    def report(self, traces: list[TraceArrays] | None = None, n_categories: int = 8):
+        """RunReport reductions per cell on the device (sl_report_batch, one launch):
+        returns (rows, cat_counts) -- rows: REPORT_DTYPE (nearest-rank p50/p90/p99
+        of TTFT in s and TPOT in ms over completed requests); cat_counts:
+        [n_sims, n_categories, 2] (total, compliant) per request category, the
+        categories taken from `traces` (TraceArrays.category), else all 0."""
+        if not self.has_outcomes:
+            raise RuntimeError("engine built without outcomes")
+        torch = self.torch
+        cat = None
+        if traces is not None:
+            c = np.concatenate([np.asarray(t.category) for t in traces]) if traces else \
+                np.zeros(0, np.int8)
+            if len(c) and (c.min() < -128 or c.max() > 127):
+                raise ValueError("categories must fit in int8")
+            cat = torch.from_numpy(np.ascontiguousarray(c, np.int8)).to(self.device)
+        rows = torch.empty(max(self.n_sims, 1) * N.REPORT_DTYPE.itemsize, dtype=torch.uint8,
+                           device=self.device)
+        counts = torch.zeros(max(self.n_sims * n_categories * 2, 1), dtype=torch.int64,
+                             device=self.device)
+        rc = N.lib().sl_report_batch(
+            C.byref(self.st), self._sims.data_ptr(), self.n_sims, C.byref(self.oc),
+            cat.data_ptr() if cat is not None else None, n_categories, rows.data_ptr(),
+            counts.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        if rc != 0:
+            raise RuntimeError(f"sl_report_batch failed with code {rc}")
+        r = rows.cpu().numpy().view(N.REPORT_DTYPE)[: self.n_sims].copy()
+        return r, counts.cpu().numpy()[: self.n_sims * n_categories * 2].reshape(
+            self.n_sims, n_categories, 2)
+
     def outcomes(self) -> dict[str, np.ndarray]:
         if not self.has_outcomes:
             raise RuntimeError("engine built without outcomes")
