@@ -202,6 +202,16 @@ int sl_report_batch(const sl_traces* traces, const sl_sim* sims, int32_t n_sims,
                     const sl_outcomes* outcomes, const int8_t* category, int32_t n_categories,
                     sl_report_row* rows, int64_t* cat_counts, void* stream);
 
+/* Cumulative SLO-met series per sim (report.summarize's `cumulative`,
+ * report.py:92): the completion times of the compliant requests, ascending,
+ * written to out_times[out_offset .. out_offset + n_out[s]) (point i of the
+ * series is (out_times[out_offset + i], i + 1)); n_out[s] = -1 for a sim
+ * without outcomes.  scratch: device buffer of at least as many u64 as
+ * out_times (the sort's second buffer).  One CTA per sim, stream-ordered. */
+int sl_cumulative_batch(const sl_traces* traces, const sl_sim* sims, int32_t n_sims,
+                        const sl_outcomes* outcomes, double* out_times, uint64_t* scratch,
+                        int64_t* n_out, void* stream);
+
 /* Number of kernels sl_run_batch launches per call (for the gpu_launches claim). */
 int sl_run_batch_launches(void);
 

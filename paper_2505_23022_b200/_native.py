@@ -173,6 +173,10 @@ def lib():
                                   C.POINTER(SlOutcomes), C.c_void_p, C.c_int32, C.c_void_p,
                                   C.c_void_p, C.c_void_p]
     L.sl_report_batch.restype = C.c_int
+    L.sl_cumulative_batch.argtypes = [C.POINTER(SlTraces), C.c_void_p, C.c_int32,
+                                      C.POINTER(SlOutcomes), C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]
+    L.sl_cumulative_batch.restype = C.c_int
     L.sl_selftest_div_small.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     L.sl_selftest_div_small.restype = C.c_int
     L.sl_abi_layout.argtypes = [C.POINTER(C.c_int64), C.c_int32]

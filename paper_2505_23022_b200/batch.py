@@ -296,6 +296,27 @@ class BatchEngine:
         return r, counts.cpu().numpy()[: self.n_sims * n_categories * 2].reshape(
             self.n_sims, n_categories, 2)
 
+    def cumulative(self) -> list[np.ndarray]:
+        """Cumulative SLO-met series per cell on the device (sl_cumulative_batch):
+        the ascending completion times of the compliant requests; point i of the
+        reference series (report.py:92) is (times[i], i + 1)."""
+        if not self.has_outcomes:
+            raise RuntimeError("engine built without outcomes")
+        torch = self.torch
+        slots = max(self.total_slots, 1)
+        times = torch.empty(slots, dtype=torch.float64, device=self.device)
+        scratch = torch.empty(slots, dtype=torch.int64, device=self.device)
+        n_out = torch.empty(max(self.n_sims, 1), dtype=torch.int64, device=self.device)
+        rc = N.lib().sl_cumulative_batch(
+            C.byref(self.st), self._sims.data_ptr(), self.n_sims, C.byref(self.oc),
+            times.data_ptr(), scratch.data_ptr(), n_out.data_ptr(),
+            torch.cuda.current_stream(self.device).cuda_stream)
+        if rc != 0:
+            raise RuntimeError(f"sl_cumulative_batch failed with code {rc}")
+        t, cnt = times.cpu().numpy(), n_out.cpu().numpy()
+        return [t[int(s["out_offset"]):int(s["out_offset"]) + int(cnt[k])].copy()
+                if cnt[k] >= 0 else np.zeros(0) for k, s in enumerate(self.sims_host)]
+
     def outcomes(self) -> dict[str, np.ndarray]:
         if not self.has_outcomes:
             raise RuntimeError("engine built without outcomes")

@@ -127,6 +127,111 @@ __global__ void __launch_bounds__(kThreads) report_kernel(const sl_traces tr, co
     cat_counts[(int64_t)si * 2 * n_cat + c] = (int64_t)cat_sm[c];
 }
 
+// Cumulative SLO-met series (report.py:92: sorted completion times of the
+// compliant requests; point i is (t_i, i + 1)).  One CTA per simulation:
+// stream-compact the compliant requests' completion times (index order) into
+// `out`, then a stable LSD radix sort of their bit patterns (non-negative
+// doubles order like their bits) between `out` and `scratch`, 8-bit digits,
+// passes whose digit is constant over the keys skipped.  Rank within a
+// 256-key tile: warp peers by __match_any_sync, warps in order through a
+// per-warp digit count table.
+constexpr int kWarps = kThreads / 32;
+
+__device__ int64_t block_compact(const int8_t* flag, const double* val, int64_t n, uint64_t* out,
+                                 unsigned* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t base = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += kThreads) {
+    const int64_t i = t0 + threadIdx.x;
+    const bool f = i < n && flag[i] != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    unsigned before = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) {
+      before += q < w ? wsum[q] : 0;
+      tot += wsum[q];
+    }
+    if (f)
+      out[base + before + __popc(bal & ((1u << lane) - 1u))] =
+          (uint64_t)__double_as_longlong(val[i]);
+    base += tot;
+    __syncthreads();
+  }
+  return base;
+}
+
+__global__ void __launch_bounds__(kThreads) cumulative_kernel(const sl_traces tr,
+                                                              const sl_sim* sims, sl_outcomes oc,
+                                                              double* out_times, uint64_t* scratch,
+                                                              int64_t* n_out) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long bucket[256];
+  __shared__ unsigned wc[kWarps][256];
+  __shared__ unsigned wsum[kWarps];
+  __shared__ int skip;
+  const sl_sim& sp = sims[blockIdx.x];
+  if (sp.out_offset < 0) {
+    if (threadIdx.x == 0) n_out[blockIdx.x] = -1;
+    return;
+  }
+  const int64_t n = tr.begin[sp.trace + 1] - tr.begin[sp.trace];
+  uint64_t* a = reinterpret_cast<uint64_t*>(out_times) + sp.out_offset;
+  uint64_t* b = scratch + sp.out_offset;
+  const int64_t c = block_compact(oc.compliant + sp.out_offset, oc.completion_time + sp.out_offset,
+                                  n, a, wsum);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int shift = 0; shift < 64; shift += 8) {
+    hist[threadIdx.x] = 0;
+    for (int q = 0; q < kWarps; ++q) wc[q][threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < c; i += kThreads) atomicAdd(&hist[(a[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive scan; a pass with one occupied digit is the identity
+      unsigned long long run = 0;
+      skip = 0;
+      for (int d = 0; d < 256; ++d) {
+        bucket[d] = run;
+        run += hist[d];
+        skip |= (int64_t)hist[d] == c;
+      }
+    }
+    __syncthreads();
+    if (skip) continue;
+    for (int64_t t0 = 0; t0 < c; t0 += kThreads) {
+      const int64_t i = t0 + threadIdx.x;
+      const bool v = i < c;
+      const uint64_t key = v ? a[i] : 0;
+      const unsigned d = (unsigned)(key >> shift) & 255u;
+      const unsigned peers = __match_any_sync(0xffffffffu, v ? d : 256u + lane);
+      if (v && lane == __ffs(peers) - 1) wc[w][d] = __popc(peers);
+      __syncthreads();
+      if (v) {
+        unsigned long long pos = bucket[d] + __popc(peers & ((1u << lane) - 1u));
+        for (int q = 0; q < w; ++q) pos += wc[q][d];
+        b[pos] = key;
+      }
+      __syncthreads();
+      unsigned add = 0;
+#pragma unroll
+      for (int q = 0; q < kWarps; ++q) {
+        add += wc[q][threadIdx.x];
+        wc[q][threadIdx.x] = 0;
+      }
+      bucket[threadIdx.x] += add;
+      __syncthreads();
+    }
+    uint64_t* t = a;
+    a = b;
+    b = t;
+  }
+  uint64_t* dst = reinterpret_cast<uint64_t*>(out_times) + sp.out_offset;
+  if (a != dst)
+    for (int64_t i = threadIdx.x; i < c; i += kThreads) dst[i] = a[i];
+  if (threadIdx.x == 0) n_out[blockIdx.x] = c;
+}
+
 }  // namespace
 
 extern "C" {
@@ -141,6 +246,17 @@ int sl_report_batch(const sl_traces* traces, const sl_sim* sims, int32_t n_sims,
   const size_t smem = sizeof(unsigned long long) * 2 * (size_t)n_categories;
   report_kernel<<<n_sims, kThreads, smem, (cudaStream_t)stream>>>(
       *traces, sims, *outcomes, category, n_categories, rows, cat_counts);
+  return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+}
+
+int sl_cumulative_batch(const sl_traces* traces, const sl_sim* sims, int32_t n_sims,
+                        const sl_outcomes* outcomes, double* out_times, uint64_t* scratch,
+                        int64_t* n_out, void* stream) {
+  if (!traces || !sims || !outcomes || !out_times || !scratch || !n_out || n_sims < 0)
+    return SL_ERR_ARG;
+  if (n_sims == 0) return SL_OK;
+  cumulative_kernel<<<n_sims, kThreads, 0, (cudaStream_t)stream>>>(*traces, sims, *outcomes,
+                                                                   out_times, scratch, n_out);
   return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
 }
 

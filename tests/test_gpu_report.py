@@ -47,8 +47,8 @@ def test_device_report_matches_summarize():
 
 
 def test_summarize_batch_matches_summarize():
-    """The batched RunReport equals summarize() on each cell's outcomes (all fields
-    but the per-request cumulative series)."""
+    """The batched RunReport equals summarize() on each cell's outcomes, every
+    field including the cumulative SLO-met series."""
     from paper_2505_23022_b200 import core
     from paper_2505_23022_b200.batch import BatchEngine
     from paper_2505_23022_b200.report import summarize, summarize_batch
@@ -77,8 +77,7 @@ def test_summarize_batch_matches_summarize():
                 slo_compliant=bool(o["compliant"][i])))
         want = summarize(outcomes, float(rows[k]["horizon"])).to_dict()
         have = got[k].to_dict()
-        want.pop("cumulative_slo_met")
-        have.pop("cumulative_slo_met")
+        assert len(have["cumulative_slo_met"]) == rows[k]["compliant"]
         assert json_equal(have, want), k
 
 
@@ -86,3 +85,31 @@ def json_equal(a, b):
     import json
 
     return json.dumps(a, sort_keys=True) == json.dumps(b, sort_keys=True)
+
+
+def test_cumulative_radix_sort_edge_cases():
+    """The device series is the sorted multiset of compliant completion times:
+    random times (all 8 radix passes live), equal times, an empty series."""
+    import torch
+
+    from paper_2505_23022_b200 import _native as N
+    from paper_2505_23022_b200.batch import BatchEngine
+
+    traces, cells = grid(n_req=400, rates=(4.0, 32.0), scales=[0.5, 2.0])
+    eng = BatchEngine(traces, cells, outcomes=True)
+    eng.launch()
+    rng = np.random.default_rng(5)
+    n = eng.total_slots
+    comp = rng.random(n) < 0.7
+    times = rng.random(n) * 10.0 ** rng.integers(-3, 4, n)
+    times[: n // 3] = 1.25  # ties
+    comp[eng.sims_host[0]["out_offset"]: eng.sims_host[0]["out_offset"] + 400] = False
+    eng._out["compliant"][:n].copy_(torch.from_numpy(comp.astype(np.int8)))
+    eng._out["completion_time"][:n].copy_(torch.from_numpy(times))
+    got = eng.cumulative()
+    for k, s in enumerate(eng.sims_host):
+        b = int(s["out_offset"])
+        m = len(traces[s["trace"]])
+        want = np.sort(times[b:b + m][comp[b:b + m]])
+        assert np.array_equal(got[k], want), k
+    assert len(got[0]) == 0
