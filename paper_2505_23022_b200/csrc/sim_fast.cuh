@@ -27,13 +27,21 @@ constexpr int kRunCap = 32 * kSlots;
 #endif
 
 // Optional per-phase cycle accounting (profiling builds only: -DSL_PHASE_PROF,
-// read back with sl_phase_prof_read).  Slots 0-7: cycles per phase, 8-13: counts.
+// read back with sl_phase_prof_read).  Slots 0-7: cycles per phase, 8-13: counts,
+// 14-15: %globaltimer (ns) at the sim's start and end, 16-19: walks, exact walks,
+// sum of W over walks, sum of W over admission scans.
 #ifdef SL_PHASE_PROF
 constexpr int kProfSims = 1 << 16;
-constexpr int kProfSlots = 14;
+constexpr int kProfSlots = 22;
+__device__ __forceinline__ unsigned long long prof_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ unsigned long long sl_prof_cycles[kProfSims][kProfSlots];
 #define SL_PROF_DECL              \
   unsigned long long prof_acc[kProfSlots] = {0}; \
+  prof_acc[14] = prof_gtime();                   \
   long long prof_t = clock64();
 #define SL_PROF_MARK(k)                 \
   {                                     \
@@ -43,6 +51,7 @@ __device__ unsigned long long sl_prof_cycles[kProfSims][kProfSlots];
   }
 #define SL_PROF_COUNT(k, v) prof_acc[k] += (v);
 #define SL_PROF_WRITE(si)                                                  \
+  prof_acc[15] = prof_gtime();                                             \
   if (lane == 0 && (si) < kProfSims)                                       \
     for (int k_ = 0; k_ < kProfSlots; ++k_) sl_prof_cycles[si][k_] = prof_acc[k_];
 #else
@@ -152,7 +161,7 @@ __device__ __forceinline__ double warp_min_nonneg(double v) {
 //     first rejection, restart after it.
 // `until` receives the time before which the walk over the remaining queue
 // provably rejects nothing (walk_pass_until), valid until the next insertion.
-__device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W,
+__device__ __forceinline__ bool spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W,
                                           int& nrej, double now, int64_t step, Acc& acc, int lane,
                                           int64_t lg_rej, int64_t cap_rej, double* bc,
                                           double& until, double& p_up) {
@@ -189,10 +198,11 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
     if (all_ok) {
       until = warp_min_nonneg(tmin);
       p_up = U;  // inflated total: bounds every prefix of the queue
-      return;
+      return false;
     }
   }
-  double* pre = bc + 32;
+  double* bcE = bc + 32;
+  double* bcT = bc + 64;
   double prefix = 0.0;
   double tmin = kInf;
   int kept = 0;
@@ -209,40 +219,45 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
       pf = r.prefill;
       tt = r.ttft;
     }
-    bc[lane] = pf;
-    __syncwarp();
     // items failing at the chunk's incoming prefix fail at any later one
     // (prefixes only grow, est is monotone in them): rejected outright
     unsigned rejm = __ballot_sync(SL_FULL, valid && fadd_(fadd_(e, prefix), pf) > tt);
-    int start = 0;
-    while (start < cnt) {
-      // assume every undecided item is kept: exact sequential prefix chain
-      double run = prefix;
-      for (int t = start; t < cnt; ++t) {
-        if (lane == 0) pre[t] = run;
-        if (!((rejm >> t) & 1u)) run = fadd_(run, bc[t]);
-      }
-      __syncwarp();
-      const double mine = pre[lane];
-      const bool rj = lane >= start && lane < cnt && !((rejm >> lane) & 1u) &&
-                      fadd_(fadd_(e, mine), pf) > tt;
-      const unsigned m = __ballot_sync(SL_FULL, rj);
-      if (m == 0) {
-        prefix = run;
-        break;
-      }
-      const int r = __ffs(m) - 1;  // first rejection; earlier items saw the true prefix
-      rejm |= 1u << r;
-      prefix = pre[r];  // a rejected item leaves the prefix unchanged
-      start = r + 1;
-      __syncwarp();
+    bc[lane] = ((rejm >> lane) & 1u) ? 0.0 : pf;  // x + 0.0 == x: rejected items add nothing
+    __syncwarp();
+    // speculative pass: the exact sequential prefix chain assuming every
+    // undecided item is kept, tested lane-parallel
+    double run = prefix, mine = 0.0;
+    for (int t = 0; t < cnt; ++t) {
+      if (lane == t) mine = run;
+      run = fadd_(run, bc[t]);
     }
+    const unsigned m = __ballot_sync(SL_FULL, valid && !((rejm >> lane) & 1u) &&
+                                                  fadd_(fadd_(e, mine), pf) > tt);
+    if (m) {
+      // first rejection r: earlier items saw the true prefix; from r on the
+      // chain runs serially with the test inline (one pass however many reject)
+      const int r = __ffs(m) - 1;
+      rejm |= 1u << r;
+      double p = __shfl_sync(SL_FULL, mine, r);  // a rejected item leaves the prefix unchanged
+      bcE[lane] = e;
+      bcT[lane] = tt;
+      __syncwarp();
+      for (int t = r + 1; t < cnt; ++t) {
+        if ((rejm >> t) & 1u) continue;
+        const double pt = bc[t];
+        const double est = fadd_(fadd_(bcE[t], p), pt);
+        if (lane == t) mine = p;
+        if (est > bcT[t])
+          rejm |= 1u << t;
+        else
+          p = fadd_(p, pt);
+      }
+      run = p;
+    }
+    prefix = run;
     const bool r_ = valid && ((rejm >> lane) & 1u);
     const bool keep = valid && !r_;
-    if (keep) {
-      const double mine = pre[lane];
-      tmin = fmin(tmin, walk_pass_until(now, mine, pf, tt, fadd_(fadd_(e, mine), pf)));
-    }
+    if (keep) tmin = fmin(tmin, walk_pass_until(now, mine, pf, tt, fadd_(fadd_(e, mine), pf)));
     const unsigned km = __ballot_sync(SL_FULL, keep);
     __syncwarp();
     if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
@@ -261,6 +276,7 @@ __device__ __forceinline__ void spec_walk(const Sim& s, const KArgs& a, bool has
   W = kept;
   until = warp_min_nonneg(tmin);
   p_up = fmul_(prefix, 1.0 + 9.313225746154785e-10);  // kept total, inflated by 2^-30
+  return true;  // the exact walk ran
 }
 
 // Cached running-set aggregates (sched_scorpio.py:117-124), warp-uniform.
@@ -747,9 +763,20 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
       if (scorpio) {
         // the walk provably rejects nothing before walk_until (no insertion
         // since it was computed, or insertions accounted for at arrival)
-        if (ttft_guard && !(SL_WALK_SKIP && now < walk_until))
-          spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej,
-                    reinterpret_cast<double*>(scr), walk_until, p_up);
+        if (ttft_guard && !(SL_WALK_SKIP && now < walk_until)) {
+          SL_PROF_COUNT(16, 1)
+          SL_PROF_COUNT(18, W)
+          const bool exact = spec_walk(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej,
+                                       cap_rej, reinterpret_cast<double*>(scr), walk_until, p_up);
+          SL_PROF_COUNT(17, exact)
+#ifdef SL_PHASE_PROF
+          {
+            const long long t_ = clock64();
+            prof_acc[exact ? 20 : 21] += (unsigned long long)(t_ - prof_t);
+          }
+#endif
+          (void)exact;
+        }
         SL_PROF_MARK(2)
         if (tpot_guard) {
           // `blocked`: every waiting request failed the admission test at a
@@ -762,6 +789,7 @@ __device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_
               g.inv_valid = true;
             }
             SL_PROF_MARK(3)
+            SL_PROF_COUNT(19, W)
             fits = spec_admit<WIDE>(s, a, has_out, W, R, sl, g, nadm, nrej, P, r_only, step, acc,
                                     lane, lg_adm, cap_adm, lg_rej, cap_rej);
             blocked = mono && nadm == 0;

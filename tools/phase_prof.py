@@ -22,7 +22,7 @@ torch.cuda.synchronize()
 res = eng.results()
 lib = N.lib()
 lib.sl_phase_prof_read.argtypes = [C.c_void_p, C.c_int32]
-out = np.zeros((eng.n_sims, 14), np.uint64)
+out = np.zeros((eng.n_sims, 22), np.uint64)
 assert lib.sl_phase_prof_read(out.ctypes.data, eng.n_sims) == eng.n_sims
 names = ["arrivals+top", "quiet", "walk", "inv_sum", "admit", "decode", "tail", "retire",
          "gen_steps", "quiet_blocks", "quiet_steps", "gen_blocked", "maxW", "maxR"]
@@ -47,3 +47,26 @@ print(f"longest sim {i}: {cyc[i].sum():.3e} cycles, steps {int(res['n_steps'][i]
 for k in range(8):
     print(f"  {names[k]:14s} {100 * cyc[i, k] / cyc[i].sum():5.1f}%")
 print("  counts", out[i, 8:].tolist())
+
+wk = out[:, 16:20].sum(axis=0).astype(np.float64)
+print("walks %d (exact %d), mean W at walk %.1f; admission scans: sum W %d (mean W %.1f over gen steps)" % (
+    wk[0], wk[1], wk[2] / max(1, wk[0]), wk[3], wk[3] / max(1, out[:, 8].sum())))
+ce, cc = out[:, 20].sum(), out[:, 21].sum()
+print("walk cycles: exact walks %.3e (%.0f per walk), certified-only %.3e (%.0f per walk)" % (
+    ce, ce / max(1, wk[1]), cc, cc / max(1, wk[0] - wk[1])))
+# occupancy timeline from the per-sim globaltimer stamps
+t0, t1 = out[:, 14].astype(np.int64), out[:, 15].astype(np.int64)
+base = t0.min()
+t0, t1 = (t0 - base) / 1e6, (t1 - base) / 1e6
+span = t1.max()
+print("timeline: makespan %.1f ms; sim-busy sum / (slots x makespan) = %.3f" % (
+    span, (t1 - t0).sum() / (148 * 16 * span)))
+for q in np.linspace(0, span, 13)[1:]:
+    print("  t=%6.1f ms  sims running %4d" % (q, int(((t0 <= q) & (t1 > q)).sum())))
+rate_idx = np.arange(eng.n_sims) // ns if eng.n_sims == nr * ns else None
+if rate_idx is not None:
+    for r in range(0, nr, max(1, nr // 8)):
+        sel = rate_idx == r
+        print("  rate %5.2f: dur %.1f-%.1f ms, start %.1f-%.1f" % (
+            grid.rates[r], (t1 - t0)[sel].min(), (t1 - t0)[sel].max(), t0[sel].min(), t0[sel].max()))
+np.save("gpurun_out/timeline.npy", np.stack([t0, t1]))
