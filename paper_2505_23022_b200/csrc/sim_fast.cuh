@@ -158,7 +158,7 @@ __device__ __forceinline__ double warp_min_nonneg(double v) {
 //     every item, no item is rejected and the queue is unchanged -- exactly.
 //  2. Otherwise the exact walk, speculative-parallel: the sequential chain
 //     assuming all undecided items are kept, lane-parallel tests, ballot for the
-//     first rejection, restart after it.
+//     first rejection; from there one serial pass with the test inline.
 // `until` receives the time before which the walk over the remaining queue
 // provably rejects nothing (walk_pass_until), valid until the next insertion.
 __device__ __forceinline__ bool spec_walk(const Sim& s, const KArgs& a, bool has_out, int& W,
