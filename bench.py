@@ -308,6 +308,67 @@ def config4_sweep(dev, reps: int = 2) -> dict:
             "mean_goodput": float(res["goodput"].mean()), "trace_gen_s": round(gen_s, 2)}
 
 
+def report_bench(grid, dev, reps: int = 3) -> dict:
+    """RunReport on the device for every cell of the config-3 sweep: the sweep with
+    per-request outcomes (41M requests), then sl_report_batch (nearest-rank
+    percentiles, per-category counts) and sl_cumulative_batch (sorted compliant
+    completion times), each timed with CUDA events."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2505_23022_b200 import _native as N
+    from paper_2505_23022_b200.batch import BatchEngine, Cell
+
+    traces = [grid.trace_for_rate(q) for q in grid.rates]
+    cells = [Cell(ri, grid.config, slo_scale=float(sc)) for ri in range(len(grid.rates))
+             for sc in grid.scales]
+    eng = BatchEngine(traces, cells, outcomes=True, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn):
+        ts = []
+        for it in range(reps + 1):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if it:
+                ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+
+    sweep_ms = timed(lambda: eng.launch(stream))
+    cat = torch.from_numpy(np.concatenate([t.category for t in traces]).astype(np.int8)).to(dev)
+    rows = torch.empty(len(cells) * N.REPORT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    counts = torch.zeros(len(cells) * 8 * 2, dtype=torch.int64, device=dev)
+    times = torch.empty(eng.total_slots, dtype=torch.float64, device=dev)
+    scratch = torch.empty(eng.total_slots, dtype=torch.int64, device=dev)
+    n_out = torch.empty(len(cells), dtype=torch.int64, device=dev)
+    lib = N.lib()
+
+    def rep():
+        assert lib.sl_report_batch(C.byref(eng.st), eng._sims.data_ptr(), eng.n_sims,
+                                   C.byref(eng.oc), cat.data_ptr(), 8, rows.data_ptr(),
+                                   counts.data_ptr(), stream.cuda_stream) == 0
+
+    def cum():
+        assert lib.sl_cumulative_batch(C.byref(eng.st), eng._sims.data_ptr(), eng.n_sims,
+                                       C.byref(eng.oc), times.data_ptr(), scratch.data_ptr(),
+                                       n_out.data_ptr(), stream.cuda_stream) == 0
+
+    rep_ms, cum_ms = timed(rep), timed(cum)
+    n_req = int(eng.total_slots)
+    return {"sims": len(cells), "requests": n_req, "sweep_with_outcomes_ms": sweep_ms,
+            "report_batch_ms": rep_ms, "cumulative_batch_ms": cum_ms,
+            "outcome_bytes_read_GBps": {
+                # report: status + compliant (2 B) + ttft/tpot (16 B, up to 8 select
+                # passes each) + category (1 B); cumulative: compliant + completion time
+                "report_1pass": n_req * 19 / (rep_ms * 1e6),
+                "cumulative_1pass": n_req * 9 / (cum_ms * 1e6)}}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -447,6 +508,8 @@ def run_ours(args) -> None:
             line["config2_plan_step"] = plan_microbench(dev, peak)
         if not args.no_config4 and world == 1:
             line["config4_noisy_predictor_sweep"] = config4_sweep(dev)
+        if not args.no_report and world == 1:
+            line["run_report_on_device"] = report_bench(grid, dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -472,6 +535,8 @@ def main() -> None:
     ap.add_argument("--no-plan", action="store_true", help="skip the config-2 plan microbench")
     ap.add_argument("--no-config4", action="store_true",
                     help="skip the config-4 sweep (16k sims, noisy predictor in the loop)")
+    ap.add_argument("--no-report", action="store_true",
+                    help="skip the device RunReport timing (config-3 sweep with outcomes)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
