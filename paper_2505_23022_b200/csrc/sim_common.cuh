@@ -143,8 +143,10 @@ __device__ __forceinline__ void insert_sorted(const Sim& s, int& W, int idx, boo
   const WRec& me = s.wr[idx];
   double dk = me.deadline, ak = me.arr;
   int32_t pk = me.pred_solo & 0x7fffffff;
+  // keys below the new one form a prefix of the list: scan chunks from the end
+  // and stop at the first chunk holding one (new arrivals mostly land late)
   int pos = 0;
-  for (int c0 = 0; c0 < W; c0 += 32) {
+  for (int c0 = (W - 1) & ~31; c0 >= 0; c0 -= 32) {
     int j = c0 + lane;
     bool lt = false;
     if (j < W) {  // primary key first; arrival / id read only on a tie
@@ -158,7 +160,11 @@ __device__ __forceinline__ void insert_sorted(const Sim& s, int& W, int idx, boo
         lt = dr != dk ? dr < dk : key_less_ldf(s, dr, r.arr, o, dk, ak, idx);
       }
     }
-    pos += __popc(__ballot_sync(SL_FULL, lt));
+    const unsigned m = __ballot_sync(SL_FULL, lt);
+    if (m) {
+      pos = c0 + __popc(m);
+      break;
+    }
   }
   // shift [pos, W) up by one, highest chunk first
   int tail = W - pos;
