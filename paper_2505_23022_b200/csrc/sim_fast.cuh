@@ -644,8 +644,12 @@ __device__ __forceinline__ void arrivals_keep_bounds(const Sim& s, int64_t n0, i
   }
   const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
   double sp = pf;  // sum of the new prefills (any order; inflated below)
+  if (kn > 1) {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) sp = fadd_(sp, __shfl_xor_sync(SL_FULL, sp, o));
+    for (int o = 16; o; o >>= 1) sp = fadd_(sp, __shfl_xor_sync(SL_FULL, sp, o));
+  } else {
+    sp = __shfl_sync(SL_FULL, pf, 0);  // one arrival (the common case)
+  }
   const double D = fadd_(fmul_(sp, inflate), fmul_(p_up, 9.313225746154785e-10));
   const double Dup = fmul_(D, 1.0 + 1.1368683772161603e-13);  // + 2^-43: rounding of D
   const double old_w = fsub_(fsub_(wu_old, Dup), fmul_(wu_old, 9.094947017729282e-13));
