@@ -300,26 +300,35 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
         // (prefixes only grow, est is monotone in them): rejected outright,
         // and the speculative chain runs over the remaining items only
         rejm = __ballot_sync(SL_FULL, valid && fadd_(fadd_(e, prefix), pf) > tt);
-        int start = 0;
-        while (start < cnt) {
+        const unsigned live = (cnt == 32 ? ~0u : (1u << cnt) - 1u) & ~rejm;
+        if (live) {
+          // speculative chain over the undecided items (assumed kept), tested
+          // lane-parallel; from the first rejection on, one serial pass with the
+          // test inline (as spec_walk in sim_fast.cuh)
+          const double pfk = ((live >> lane) & 1u) ? pf : 0.0;  // x + 0.0 == x
           double run = prefix, mine = 0.0;
-          for (int t = start; t < cnt; ++t) {
-            if ((rejm >> t) & 1u) continue;
-            const double x = bcast(pf, t);
+          for (int t = __ffs(live) - 1; t < cnt; ++t) {
+            const double x = bcast(pfk, t);
             if (lane == t) mine = run;
             run = fadd_(run, x);
           }
-          const bool rj = lane >= start && lane < cnt && !((rejm >> lane) & 1u) &&
-                          fadd_(fadd_(e, mine), pf) > tt;
-          const unsigned m = __ballot_sync(SL_FULL, rj);
-          if (m == 0) {
-            prefix = run;
-            break;
+          const unsigned m = __ballot_sync(SL_FULL, ((live >> lane) & 1u) &&
+                                                        fadd_(fadd_(e, mine), pf) > tt);
+          if (m) {
+            const int r = __ffs(m) - 1;
+            rejm |= 1u << r;
+            double q = bcast(mine, r);  // a rejected item leaves the prefix unchanged
+            for (int t = r + 1; t < cnt; ++t) {
+              if ((rejm >> t) & 1u) continue;
+              const double x = bcast(pf, t), et = bcast(e, t), tt_t = bcast(tt, t);
+              if (fadd_(fadd_(et, q), x) > tt_t)
+                rejm |= 1u << t;
+              else
+                q = fadd_(q, x);
+            }
+            run = q;
           }
-          const int r = __ffs(m) - 1;
-          rejm |= 1u << r;
-          prefix = bcast(mine, r);
-          start = r + 1;
+          prefix = run;
         }
       }
       const bool rj = valid && ((rejm >> lane) & 1u);
