@@ -149,6 +149,40 @@ __device__ __forceinline__ double warp_min_nonneg(double v) {
   return __longlong_as_double((long long)(((uint64_t)hi << 32) | lo));
 }
 
+// Certified pass over chunks [c_from, W) of the queue given an upper bound U of
+// the prefix before c_from (see spec_walk): true iff no item can be rejected;
+// tmin / U accumulate the walk bound and the inflated running prefix bound.
+__device__ __forceinline__ bool cert_scan(const Sim& s, double now, int W, int c_from, int lane,
+                                          double& U, double& tmin) {
+  const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
+  bool all_ok = true;
+  for (int c0 = c_from; c0 < W && all_ok; c0 += 32) {
+    const int j = c0 + lane;
+    const bool valid = j < W;
+    double e = 0.0, pf = 0.0, tt = 0.0;
+    if (valid) {
+      const WRec& r = s.wr[s.wl[j]];
+      e = fsub_(now, r.arr);
+      pf = r.prefill;
+      tt = r.ttft;
+    }
+    double v = pf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(SL_FULL, v, o);
+      if (lane >= o) v = fadd_(v, y);
+    }
+    double excl = __shfl_up_sync(SL_FULL, v, 1);
+    if (lane == 0) excl = 0.0;
+    const double Uj = fmul_(fadd_(U, excl), inflate);
+    const double est0 = fadd_(fadd_(e, Uj), pf);
+    all_ok = __all_sync(SL_FULL, !valid || est0 <= tt);
+    if (valid) tmin = fmin(tmin, walk_pass_until(now, Uj, pf, tt, est0));
+    U = fmul_(fadd_(U, __shfl_sync(SL_FULL, v, 31)), inflate);
+  }
+  return all_ok;
+}
+
 // TTFT prefix walk over wl[0, W) in list order (ttft_guard sched_scorpio.py:196-205;
 // early_reject sched_baselines.py:95-103).
 //  1. Certified pass: an upper bound U_j of the sequential prefix (warp scan in
@@ -166,36 +200,11 @@ __device__ __forceinline__ bool spec_walk(const Sim& s, const KArgs& a, bool has
                                           int64_t lg_rej, int64_t cap_rej, double* bc,
                                           double& until, double& p_up) {
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  if (W < (1 << 20)) {
-    const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
+  const bool certifiable = W < (1 << 20);
+  if (certifiable) {
     double U = 0.0;
     double tmin = kInf;
-    bool all_ok = true;
-    for (int c0 = 0; c0 < W && all_ok; c0 += 32) {
-      const int j = c0 + lane;
-      const bool valid = j < W;
-      double e = 0.0, pf = 0.0, tt = 0.0;
-      if (valid) {
-        const WRec& r = s.wr[s.wl[j]];
-        e = fsub_(now, r.arr);
-        pf = r.prefill;
-        tt = r.ttft;
-      }
-      double v = pf;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(SL_FULL, v, o);
-        if (lane >= o) v = fadd_(v, y);
-      }
-      double excl = __shfl_up_sync(SL_FULL, v, 1);
-      if (lane == 0) excl = 0.0;
-      const double Uj = fmul_(fadd_(U, excl), inflate);
-      const double est0 = fadd_(fadd_(e, Uj), pf);
-      all_ok = __all_sync(SL_FULL, !valid || est0 <= tt);
-      if (valid) tmin = fmin(tmin, walk_pass_until(now, Uj, pf, tt, est0));
-      U = fmul_(fadd_(U, __shfl_sync(SL_FULL, v, 31)), inflate);
-    }
-    if (all_ok) {
+    if (cert_scan(s, now, W, 0, lane, U, tmin)) {
       until = warp_min_nonneg(tmin);
       p_up = U;  // inflated total: bounds every prefix of the queue
       return false;
@@ -272,6 +281,25 @@ __device__ __forceinline__ bool spec_walk(const Sim& s, const KArgs& a, bool has
     __syncwarp();
     kept += __popc(km);
     nrej += __popc(rejm);
+    if (rejm && certifiable && c0 + 32 < W) {
+      // rejections come first in deadline order: if the rest of the queue is
+      // certified from the exact prefix here, it only moves down the list
+      double U = prefix, tc = tmin;
+      if (cert_scan(s, now, W, c0 + 32, lane, U, tc)) {
+        for (int c1 = c0 + 32; c1 < W; c1 += 32) {
+          const bool v1 = c1 + lane < W;
+          const int i1 = v1 ? s.wl[c1 + lane] : 0;
+          __syncwarp();
+          if (v1) s.wl[kept + lane] = i1;
+          __syncwarp();
+          kept += min(32, W - c1);
+        }
+        W = kept;
+        until = warp_min_nonneg(tc);
+        p_up = U;
+        return true;
+      }
+    }
   }
   W = kept;
   until = warp_min_nonneg(tmin);
