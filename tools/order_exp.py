@@ -21,6 +21,10 @@ if z is not None:
     for k in list(z.keys()):
         if k.startswith("order_"):
             orders[k] = z[k]
+if len(sys.argv) > 2:
+    z2 = np.load(sys.argv[2])
+    for k in z2.keys():
+        orders[k] = z2[k]
 rng = np.random.default_rng(0)
 orders["random"] = rng.permutation(eng.n_sims)
 orders["rate_desc"] = orders["current"][::-1].copy()
