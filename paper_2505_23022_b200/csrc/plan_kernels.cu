@@ -518,19 +518,25 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
   seg_guard_admit(st, cfg, out, seg, threadIdx.x & 31);
 }
 
-// Large batches: one warp per 32 segments.  The order-dependent Neumaier folds
+// Large batches: one warp per kPlanGroup segments.  The order-dependent Neumaier folds
 // (sum(1/slo) over running, sched_scorpio.py:121; vbs over running + admitted,
 // :312-315) run lane-per-segment -- one warp instruction advances 32 folds
 // instead of 32 lanes repeating one -- and the walk / admission scan run
 // warp-per-segment in between (seg_guard_admit<true>).
-__global__ void __launch_bounds__(128) guard_admit_group_kernel(const sl_plan_state st,
-                                                                const sl_plan_config cfg,
-                                                                sl_plan_out out) {
+#ifndef SL_PLAN_GROUP
+#define SL_PLAN_GROUP 16  // segments per warp (measured: 16 with 7 blocks/SM beats 32, 8 and 4)
+#endif
+#ifndef SL_PLAN_GROUP_BLOCKS
+#define SL_PLAN_GROUP_BLOCKS 7  // <= 72 registers: 28 warps/SM
+#endif
+constexpr int kPlanGroup = SL_PLAN_GROUP;
+__global__ void __launch_bounds__(128, SL_PLAN_GROUP_BLOCKS) guard_admit_group_kernel(
+    const sl_plan_state st, const sl_plan_config cfg, sl_plan_out out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int seg0 = warp * 32;
+  const int seg0 = warp * kPlanGroup;
   if (seg0 >= st.n_segments) return;
-  const int nseg = min(32, st.n_segments - seg0);
+  const int nseg = min(kPlanGroup, st.n_segments - seg0);
   const int my = seg0 + lane;
   const bool mine = lane < nseg;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -728,7 +734,7 @@ int sl_guard_admit_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_
   if ((cfg->flags & SL_FLAG_TTFT_GUARD) && !out->perm) return SL_ERR_ARG;
   if (st->n_segments == 0) return SL_OK;
   if (st->n_segments >= plan_group_min()) {
-    guard_admit_group_kernel<<<warps_grid((st->n_segments + 31) / 32, 128), 128, 0,
+    guard_admit_group_kernel<<<warps_grid((st->n_segments + kPlanGroup - 1) / kPlanGroup, 128), 128, 0,
                                (cudaStream_t)stream>>>(*st, *cfg, *out);
     return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
   }
