@@ -113,3 +113,25 @@ def test_cumulative_radix_sort_edge_cases():
         want = np.sort(times[b:b + m][comp[b:b + m]])
         assert np.array_equal(got[k], want), k
     assert len(got[0]) == 0
+
+
+def test_report_with_no_completions():
+    """Cells whose SLOs reject everything: NaN percentiles, n_completed 0, an
+    empty cumulative series, per-category totals still counted."""
+    from paper_2505_23022_b200.batch import BatchEngine
+    from paper_2505_23022_b200.report import summarize_batch
+
+    traces, cells = grid(n_req=300, rates=(32.0,), scales=[1e-4, 1.0])
+    eng = BatchEngine(traces, cells, outcomes=True)
+    eng.launch()
+    rows, counts = eng.report(traces)
+    series = eng.cumulative()
+    rep = summarize_batch(eng, traces)
+    res = eng.results()
+    for k in range(len(cells)):
+        if res[k]["completed"] == 0:
+            assert rows[k]["n_completed"] == 0
+            assert np.isnan(rows[k]["ttft_p50"]) and np.isnan(rows[k]["tpot_ms_p99"])
+            assert len(series[k]) == 0 and rep[k].cumulative == []
+        assert counts[k, :, 0].sum() == len(traces[cells[k].trace])
+    assert (res["completed"] == 0).any()
