@@ -825,6 +825,13 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
     int64_t max_blocks = (int64_t)sms * per_sm;
     return (unsigned)(blocks < max_blocks ? blocks : max_blocks);
   };
+  if (const char* e = getenv("SL_CARVEOUT")) {  // experiments: shared-memory carveout (percent)
+    const int pct = atoi(e);
+    cudaFuncSetAttribute((const void*)sl_sim_fast_kernel<true, false>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute((const void*)sl_sim_fast_kernel<true, true>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  }
   if (mode == SL_MODE_AUTO) {
     if (!a.has_log) {
       if (a.has_out)
