@@ -9,6 +9,11 @@
 #include "scorpio_b200.h"
 #include "sl_device.cuh"
 
+#ifndef SL_PREFETCH
+#define SL_PREFETCH 1  // prefetch the next arriving request's WRec into L1 (measured -1%;
+                        // 2: also its id / output length, measured +3%)
+#endif
+
 namespace sl {
 
 
@@ -282,6 +287,15 @@ __device__ __forceinline__ void process_arrivals(const Sim& s, int& W, int64_t& 
     next += k;
     next_t = next < s.n ? (s.factor == 1.0 ? s.arrival[next] : s.wr[next].arr) : kInf;
   }
+#if SL_PREFETCH
+  // the next request's WRec (first touched at its arrival): start the L1 fill now
+  if (lane == 0 && next < s.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(s.wr + next));
+#if SL_PREFETCH >= 2
+  // and its id / output length (read when it is admitted)
+  if (lane == 1 && next < s.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(s.id + next));
+  if (lane == 2 && next < s.n) asm volatile("prefetch.global.L1 [%0];" ::"l"(s.true_out + next));
+#endif
+#endif
 }
 
 // Per-lane accumulators folded into the result row at the end.
