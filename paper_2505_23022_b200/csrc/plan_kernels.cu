@@ -641,6 +641,80 @@ __global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_confi
   seg_credit_select(st, cfg, out, use_seg_min, seg, threadIdx.x & 31);
 }
 
+// Few, large segments (the config-2 stress shape): one 1024-thread CTA per
+// segment instead of one warp, tiles of 1024 entries, batch positions by a
+// CTA-wide ballot scan -- the same per-entry arithmetic as seg_credit_select.
+constexpr int kSelCta = 1024;
+__global__ void __launch_bounds__(kSelCta) credit_select_cta_kernel(const sl_plan_state st,
+                                                                    const sl_plan_config cfg,
+                                                                    sl_plan_out out,
+                                                                    int use_seg_min) {
+  __shared__ unsigned wcnt[kSelCta / 32];
+  __shared__ unsigned long long smin;
+  const int seg = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool credit = cfg.flags & SL_FLAG_TPOT_GUARD;
+  const int64_t rb = st.r_begin[seg];
+  const int R = (int)(st.r_begin[seg + 1] - rb);
+  const int E = st.credit_exp[seg];
+  if (threadIdx.x == 0) smin = ~0ull;
+  __syncthreads();
+  if (credit) {
+    if (use_seg_min) {
+      if (threadIdx.x == 0) smin = out.seg_min_fixed[seg];
+    } else {
+      uint64_t m = ~0ull;
+      for (int j = threadIdx.x; j < R; j += kSelCta) {
+        const uint64_t S = slo_fixed<false>(st.r_tpot[rb + j], E);
+        m = S < m ? S : m;
+      }
+      m = warp_min_cred<false>(m);
+      if (lane == 0) atomicMin(&smin, (unsigned long long)m);
+    }
+  }
+  __syncthreads();
+  const uint64_t MIN = smin;
+  int nb = 0;
+  for (int c0 = 0; c0 < R; c0 += kSelCta) {
+    const int j = c0 + threadIdx.x;
+    bool b = false;
+    if (j < R) {
+      const int64_t r = rb + j;
+      const bool ex = st.r_exclude && st.r_exclude[r];
+      uint64_t N = st.r_credit[r];
+      if (!ex) {
+        if (credit) {
+          const uint64_t S = slo_fixed<false>(st.r_tpot[r], E);
+          N += MIN;
+          b = N >= S;
+          if (b) N -= S;
+        } else {
+          b = true;
+        }
+      }
+      out.r_credit_out[r] = N;
+    }
+    const unsigned bm = __ballot_sync(SL_FULL, b);
+    if (lane == 0) wcnt[w] = __popc(bm);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int q = 0; q < kSelCta / 32; ++q) {
+      before += q < w ? (int)wcnt[q] : 0;
+      tot += (int)wcnt[q];
+    }
+    if (j < R) {
+      out.r_batch[rb + j] = b;
+      out.r_pos[rb + j] = b ? nb + before + __popc(bm & lanemask_lt()) : -1;
+    }
+    nb += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out.seg_counts[4 * seg + 3] = nb;
+}
+
+// Segment count below which credit select runs one CTA per segment.
+constexpr int kSelCtaMaxSegments = 64;
+
 // ---- the whole plan_step in one launch (segments of <= 32 waiting items):
 // sort, guard + admission, credit select back to back in one warp; the stages
 // hand over through the segment's own global slices (L1-resident), so inputs
@@ -749,8 +823,12 @@ int sl_credit_select_batch(const sl_plan_state* st, const sl_plan_config* cfg, s
       !out->seg_counts || (use_seg_min && !out->seg_min_fixed))
     return SL_ERR_ARG;
   if (st->n_segments == 0) return SL_OK;
-  credit_select_kernel<<<warps_grid(st->n_segments, 128), 128, 0, (cudaStream_t)stream>>>(
-      *st, *cfg, *out, use_seg_min);
+  if (st->n_segments <= kSelCtaMaxSegments)
+    credit_select_cta_kernel<<<st->n_segments, kSelCta, 0, (cudaStream_t)stream>>>(
+        *st, *cfg, *out, use_seg_min);
+  else
+    credit_select_kernel<<<warps_grid(st->n_segments, 128), 128, 0, (cudaStream_t)stream>>>(
+        *st, *cfg, *out, use_seg_min);
   return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
 }
 
