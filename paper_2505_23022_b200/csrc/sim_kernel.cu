@@ -6,12 +6,15 @@
 // Mapping:
 //  * one warp owns one simulation at a time and pulls the next one from a
 //    device work counter over a host-ordered (longest-first) schedule;
-//  * per-request arrival-time constants live in a 64-byte WRec, written once
-//    when the request becomes visible; the waiting queue is an int32 index
-//    list kept in LDF order by warp-parallel rank+shift insertion;
-//  * the running set is a positional SoA (32-byte RRec per entry, admission
-//    order) so credit updates, emits and retire compaction are coalesced
-//    lane-parallel passes; batch compaction = ballot + popc;
+//  * per-request arrival-time constants live in a 64-byte WRec, built for
+//    every request of every sim by wrec_prepass_kernel ahead of the
+//    simulation kernels; the waiting queue is an int32 index list kept in LDF
+//    order by warp-parallel rank+shift insertion;
+//  * the running set: in registers in the fast kernels (sim_fast.cuh: entry j
+//    in lane j % 32, slot j / 32, up to 64 entries); in this general kernel a
+//    positional SoA (32-byte RRec per entry, admission order), so credit
+//    updates, emits and retire compaction are coalesced lane-parallel passes;
+//    batch compaction = ballot + popc;
 //  * the order-dependent fp64 chains (TTFT prefix walk, Neumaier aggregates,
 //    greedy admission scan) run warp-uniformly over register-staged chunks
 //    (one chunk load per 32 items, values broadcast with shuffles) so every
