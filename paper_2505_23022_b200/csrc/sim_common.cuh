@@ -148,9 +148,29 @@ __device__ __forceinline__ void insert_sorted(const Sim& s, int& W, int idx, boo
   const WRec& me = s.wr[idx];
   double dk = me.deadline, ak = me.arr;
   int32_t pk = me.pred_solo & 0x7fffffff;
+  int pos = 0;
+  if (sjf && W > 64) {
+    // SJF arrivals land anywhere: 32-ary search (32 probes per round) over the
+    // sorted list, then one chunk.  Invariant: keys below lo are smaller,
+    // keys from hi on larger than the new one.
+    auto less_new = [&](int j) {
+      const int o = s.wl[j];
+      const int32_t pr = s.wr[o].pred_solo & 0x7fffffff;
+      return pr != pk ? pr < pk : key_less_sjf(s, pr, s.wr[o].arr, o, pk, ak, idx);
+    };
+    int lo = 0, hi = W;
+    while (hi - lo > 32) {
+      const int stride = (hi - lo + 31) / 32;
+      const int q = lo + lane * stride;
+      const int cnt = __popc(__ballot_sync(SL_FULL, q < hi && less_new(q)));
+      const int nhi = lo + cnt * stride;
+      lo = cnt ? lo + (cnt - 1) * stride + 1 : lo;
+      hi = nhi < hi ? nhi : hi;
+    }
+    pos = lo + __popc(__ballot_sync(SL_FULL, lo + lane < hi && less_new(lo + lane)));
+  } else {
   // keys below the new one form a prefix of the list: scan chunks from the end
   // and stop at the first chunk holding one (new arrivals mostly land late)
-  int pos = 0;
   for (int c0 = (W - 1) & ~31; c0 >= 0; c0 -= 32) {
     int j = c0 + lane;
     bool lt = false;
@@ -170,6 +190,7 @@ __device__ __forceinline__ void insert_sorted(const Sim& s, int& W, int idx, boo
       pos = c0 + __popc(m);
       break;
     }
+  }
   }
   // shift [pos, W) up by one, highest chunk first
   int tail = W - pos;
