@@ -84,9 +84,11 @@ __device__ void ttft_walk(const Sim& s, const KArgs& a, bool has_out, int& W, in
 }
 
 // Append waiting items wl[0, take) to the running list in order (admit-all /
-// admit_fcfs) and shift the waiting list down.  Returns the Neumaier prefill sum.
+// admit_fcfs) and drop them from the front of the waiting list by advancing
+// its base (each request enters the list once, so base + W never passes the
+// sim's n slots).  Returns the Neumaier prefill sum.
 template <bool WIDE>
-__device__ void admit_prefix(const Sim& s, const KArgs& a, int& W, int& R, int take, int& nadm,
+__device__ void admit_prefix(Sim& s, const KArgs& a, int& W, int& R, int take, int& nadm,
                              PySum& P, int64_t step, Acc& acc, int lane, int64_t log_adm_base,
                              int64_t log_cap) {
   for (int c0 = 0; c0 < take; c0 += 32) {
@@ -117,19 +119,10 @@ __device__ void admit_prefix(const Sim& s, const KArgs& a, int& W, int& R, int t
     for (int t = 0; t < cnt; ++t) ps_add(P, bcast(pf, t));
   }
   __syncwarp();
-  // shift remaining waiting items down by `take`
-  int rest = W - take;
-  for (int c0 = 0; c0 < rest; c0 += 32) {
-    int j = c0 + lane;
-    int v = 0;
-    if (j < rest) v = s.wl[take + j];
-    __syncwarp();
-    if (j < rest) s.wl[j] = v;
-    __syncwarp();
-  }
+  s.wl += take;
   R += take;
   nadm += take;
-  W = rest;
+  W -= take;
 }
 
 template <bool WIDE>
@@ -152,7 +145,7 @@ __device__ cred_t<WIDE> running_min_S(const Sim& s, int R, int lane) {
 }
 
 template <bool WIDE>
-__device__ void run_sim(const Sim& s, const KArgs& a, bool has_out, int sim_index, int lane) {
+__device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int lane) {
   const int64_t n = s.n;
   const sl_cost& C = s.cost;
   const bool scorpio = s.policy == SL_POLICY_SCORPIO;
