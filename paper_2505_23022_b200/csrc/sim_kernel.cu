@@ -381,6 +381,7 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
     const bool credit = scorpio && tpot_guard;
     const bool decode_all = !credit && !(s.policy != SL_POLICY_SCORPIO &&
                                          (s.flags & SL_FLAG_PREFILL_PRIORITY) && nadm > 0);
+    bool batch_ret = false;  // a batched entry emitted its last token
     if (credit || decode_all) {
       for (int c0 = 0; c0 < R0; c0 += 32) {
         int j = c0 + lane;
@@ -417,6 +418,7 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
           blen += r.cur_len;
           r.cur_len += 1;  // token emit (simengine.py:243-245); l_avg already taken
           r.rem -= 1;
+          batch_ret |= r.rem <= 0;
           int64_t rid = s.id[s.rl[j]];
           bhash += batch_hid((uint64_t)rid);
           if (lg_bat >= 0 && pos < cap_bat) a.log.batch_ids[lg_bat + pos] = rid;
@@ -516,6 +518,22 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
     }
 
     // ---- emits for fresh entries + retirement (simengine.py:240-271)
+    // Only entries that emitted this step can finish: batched ones (batch_ret)
+    // and the admitted (remaining 1).  Without any, just the first tokens.
+    bool may_ret = batch_ret;
+    for (int j = R0 + lane; j < R; j += 32) may_ret |= s.rr[j].rem <= 1;
+    if (!__any_sync(SL_FULL, may_ret)) {
+      for (int j = R0 + lane; j < R; j += 32) {
+        RRec& r = s.rr[j];
+        r.cur_len += 1;
+        r.rem -= 1;
+        s.first_emit[s.rl[j]] = end;
+      }
+      __syncwarp();
+      now = end;
+      step++;
+      continue;
+    }
     int keptR = 0;
     for (int c0 = 0; c0 < R; c0 += 32) {
       int j = c0 + lane;
