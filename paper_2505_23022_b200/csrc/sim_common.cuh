@@ -49,6 +49,7 @@ struct Workspace {  // SoA regions over all request slots
   uint64_t* rNhi;    // wide credits: per running position
   uint64_t* rShi;
   double* first_emit;  // per request
+  uint32_t* rh;        // batch_hid(id) per running position (general kernel)
 };
 
 __host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -74,11 +75,13 @@ __host__ __device__ inline Workspace carve(void* base, int64_t slots) {
   w.rShi = (uint64_t*)(p + off);
   off = align256(off + slots * 8);
   w.first_emit = (double*)(p + off);
+  off = align256(off + slots * 8);
+  w.rh = (uint32_t*)(p + off);
   return w;
 }
 
 __host__ __device__ inline int64_t workspace_bytes(int64_t slots) {
-  return 256 + 8 * 256 + align256(slots * 4) * 2 + align256(slots * 64) + align256(slots * 32) +
+  return 256 + 8 * 256 + align256(slots * 4) * 3 + align256(slots * 64) + align256(slots * 32) +
          align256(slots * 8) * 4;
 }
 
@@ -114,6 +117,7 @@ struct Sim {
   // workspace slices
   int32_t* wl;
   int32_t* rl;
+  uint32_t* rh;
   WRec* wr;
   RRec* rr;
   uint64_t* wShi;
@@ -235,6 +239,7 @@ __device__ __forceinline__ Sim make_sim(const KArgs& a, const Workspace& ws, int
   int64_t o = sp.ws_offset;
   s.wl = ws.wl + o;
   s.rl = ws.rl + o;
+  s.rh = ws.rh + o;
   s.wr = ws.wr + o;
   s.rr = ws.rr + o;
   s.wShi = ws.wShi + o;

@@ -112,6 +112,7 @@ __device__ void admit_prefix(Sim& s, const KArgs& a, int& W, int& R, int take, i
         s.rShi[R + j] = s.wShi[idx];
       }
       int64_t rid = s.id[idx];
+      s.rh[R + j] = batch_hid((uint64_t)rid);
       acc.dig += digest_item((uint64_t)step, 0, (uint32_t)(nadm + j), (uint64_t)rid);
       if (log_adm_base >= 0 && nadm + j < log_cap) a.log.adm_ids[log_adm_base + nadm + j] = rid;
     }
@@ -341,6 +342,7 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
                 s.rShi[R + q] = (uint64_t)(Sc >> 64);
               }
               int64_t rid = s.id[idx];
+              s.rh[R + q] = batch_hid((uint64_t)rid);
               acc.dig += digest_item((uint64_t)step, 0, (uint32_t)(nadm + q), (uint64_t)rid);
               if (lg_adm >= 0 && nadm + q < cap_adm) a.log.adm_ids[lg_adm + nadm + q] = rid;
             }
@@ -419,9 +421,8 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
           r.cur_len += 1;  // token emit (simengine.py:243-245); l_avg already taken
           r.rem -= 1;
           batch_ret |= r.rem <= 0;
-          int64_t rid = s.id[s.rl[j]];
-          bhash += batch_hid((uint64_t)rid);
-          if (lg_bat >= 0 && pos < cap_bat) a.log.batch_ids[lg_bat + pos] = rid;
+          bhash += s.rh[j];  // batch_hid(id), kept per running position
+          if (lg_bat >= 0 && pos < cap_bat) a.log.batch_ids[lg_bat + pos] = s.id[s.rl[j]];
         }
         nbatch += __popc(bm);
       }
@@ -540,11 +541,13 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
       bool valid = j < R;
       RRec r;
       int idx = 0;
+      uint32_t hid = 0;
       uint64_t nhi = 0, shi = 0;
       bool ret = false;
       if (valid) {
         r = s.rr[j];
         idx = s.rl[j];
+        hid = s.rh[j];
         if constexpr (WIDE) {
           nhi = s.rNhi[j];
           shi = s.rShi[j];
@@ -562,6 +565,7 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
         int q = keptR + __popc(km & lanemask_lt());
         s.rr[q] = r;
         s.rl[q] = idx;
+        s.rh[q] = hid;
         if constexpr (WIDE) {
           s.rNhi[q] = nhi;
           s.rShi[q] = shi;
