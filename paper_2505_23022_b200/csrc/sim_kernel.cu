@@ -296,7 +296,7 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
               bool lt = !has_min || cand < min_d;
               double minp = lt ? cand : min_d;
               double V = fmul_(minp, fadd_(inv, icand));
-              double L = fdiv_((double)(lens + clen), (double)(n_run + 1));
+              double L = div_small((double)(lens + clen), (int)(n_run + 1));  // exact int / int
               double est = tpot_estimate(C, V, L, cpred);
               double thr = (r_only && has_min) ? min_d : minp;
               if (est <= thr) {
@@ -470,7 +470,7 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
     double prefill_s = ps_result(P);
     double decode_s = 0.0;
     int64_t bl = warp_sum_i64(blen);
-    if (nbatch > 0) decode_s = itl(C, nbatch, fdiv_((double)bl, (double)nbatch));
+    if (nbatch > 0) decode_s = itl(C, nbatch, div_small((double)bl, nbatch));  // exact int / int
     double end = fadd_(fadd_(now, prefill_s), decode_s);
     acc.dig += acc.dig_rej;
     bhash = __reduce_add_sync(SL_FULL, bhash);
