@@ -447,9 +447,13 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
 }
 
 // Append waiting items wl[0, take) to the running set in order (admit-all,
-// sched_scorpio.py:295-304, and admit_fcfs, sched_baselines.py:49-60).
+// sched_scorpio.py:295-304, and admit_fcfs, sched_baselines.py:49-60), then
+// drop them from the front of the waiting list by advancing its base (each
+// request enters the list once, so base + W stays within the sim's n slots).
+// `s` is this thread's own copy of the Sim (never called by the hot kernel,
+// whose Sim is shared in shared memory).
 template <bool WIDE>
-__device__ __forceinline__ bool append_prefix(const Sim& s, const KArgs& a, int& W, int& R,
+__device__ __forceinline__ bool append_prefix(Sim& s, const KArgs& a, int& W, int& R,
                               Slot<WIDE> (&sl)[kSlots], Agg<WIDE>& g, int take, int& nadm,
                               PySum& P, int64_t step, Acc& acc, int lane, int64_t lg_adm,
                               int64_t cap_adm) {
@@ -499,17 +503,9 @@ __device__ __forceinline__ bool append_prefix(const Sim& s, const KArgs& a, int&
     }
   }
   __syncwarp();
-  int rest = W - take;
-  for (int c0 = 0; c0 < rest; c0 += 32) {
-    int j = c0 + lane;
-    int v = 0;
-    if (j < rest) v = s.wl[take + j];
-    __syncwarp();
-    if (j < rest) s.wl[j] = v;
-    __syncwarp();
-  }
+  s.wl += take;
   nadm += take;
-  W = rest;
+  W -= take;
   if (take) g.inv_valid = false;
   return true;
 }
@@ -695,7 +691,7 @@ __device__ __forceinline__ void arrivals_keep_bounds(const Sim& s, int64_t n0, i
 // both guards, no decision log -- so the hot kernel carries no baseline,
 // ablation or logging code (smaller instruction footprint, fewer registers).
 template <bool WIDE, bool HOT = false>
-__device__ __forceinline__ void run_fast(const Sim& s, const KArgs& a, bool has_out, int si, int lane,
+__device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, int si, int lane,
                          Slot<WIDE>* scr) {
   const int64_t n = s.n;
   const sl_cost& C = s.cost;

@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(32 * kFastWarps, HOT ? SL_HOT_MIN_BLOCKS : 1) 
       __syncwarp();
       if (lane == 0) sim_sm[warp] = make_sim(a, ws, si);
       __syncwarp();
-      const Sim& s = sim_sm[warp];
+      Sim& s = sim_sm[warp];  // read-only on the hot path (no append_prefix)
 #else
       Sim s = make_sim(a, ws, si);
 #endif
