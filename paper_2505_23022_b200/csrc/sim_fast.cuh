@@ -585,7 +585,7 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
                                             Agg<WIDE>& g, double& now, int64_t& step,
                                             int64_t& n_plans, int64_t& req_steps, double next_t,
                                             double walk_until, bool has_h, Acc& acc, int lane,
-                                            Slot<WIDE>* scr) {
+                                            Slot<WIDE>* scr, bool all = false) {
   const sl_cost& C = s.cost;
   const double horizon = has_h ? s.horizon : __longlong_as_double(0x7ff0000000000000LL);
   // a step runs while now < lim (next arrival, horizon, walk bound: all strict)
@@ -603,8 +603,8 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   bool ret = false;
   while (R > 0 && R <= 32 && now < lim) {
     const cred_t<WIDE> N = sl[0].N + g.Smin;
-    const bool b = live && N >= sl[0].S;
-    if (live) sl[0].N = b ? N - sl[0].S : N;
+    const bool b = live && (all || N >= sl[0].S);  // all: decode-all policies, no credits
+    if (live && !all) sl[0].N = b ? N - sl[0].S : N;
     const int nb = __popc(__ballot_sync(SL_FULL, b));
     const unsigned blen = __reduce_add_sync(SL_FULL, b ? (unsigned)sl[0].cur_len : 0u);
     const unsigned bh = __reduce_add_sync(SL_FULL, b ? hh : 0u);
@@ -757,11 +757,12 @@ __device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, i
     bool ret;  // entries retire at the end of step `step - 1` (at `now`)
     // quiet / blocked steps: nothing can be admitted or rejected (W == 0, or
     // the admission scan provably fails and the walk provably passes)
-    if (credit && !logging && R > 0 && R <= 32 && (W == 0 || (blocked && now < walk_until))) {
+    if (!logging && R > 0 && R <= 32 &&
+        (credit ? (W == 0 || (blocked && now < walk_until)) : W == 0)) {
       SL_PROF_COUNT(9, 1)
       SL_PROF_COUNT(10, -step)
       ret = quiet_steps<WIDE>(s, a, has_out, sl, R, W, g, now, step, n_plans, req_steps, next_t,
-                              W > 0 ? walk_until : kInf, has_h, acc, lane, scr);
+                              W > 0 ? walk_until : kInf, has_h, acc, lane, scr, !credit);
       SL_PROF_COUNT(10, step)
       SL_PROF_MARK(1)
     } else {
