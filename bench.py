@@ -369,6 +369,45 @@ def report_bench(grid, dev, reps: int = 3) -> dict:
                 "cumulative_1pass": n_req * 9 / (cum_ms * 1e6)}}
 
 
+def baselines_bench(grid, dev) -> dict:
+    """the config-3 grid under each reference policy
+    (sched_baselines.py greedy / sjf / early_reject and scorpio) on the same
+    traces and engine: sweep time, request-steps/s, mean goodput, and the
+    per-cell goodput ratio scorpio / baseline (the paper's Fig-4 quantity)."""
+    from dataclasses import replace
+
+    import torch
+
+    from paper_2505_23022_b200.batch import BatchEngine, Cell
+
+    traces = [grid.trace_for_rate(q) for q in grid.rates]
+    stream = torch.cuda.current_stream(dev)
+    out, good = {}, {}
+    for pol in ("scorpio", "greedy", "sjf", "early_reject"):
+        cfg = replace(grid.config, policy=pol)
+        cells = [Cell(ri, cfg, slo_scale=float(sc)) for ri in range(len(grid.rates))
+                 for sc in grid.scales]
+        eng = BatchEngine(traces, cells, device=dev)
+        eng.launch(stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.launch(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        r = eng.results()
+        ms = e0.elapsed_time(e1)
+        rs = int(r["request_steps"].sum())
+        good[pol] = r["goodput"].astype(np.float64)
+        out[pol] = {"ms": ms, "request_steps": rs, "request_steps_per_s": rs / (ms / 1e3),
+                    "mean_goodput": float(good[pol].mean())}
+    for pol in ("greedy", "sjf", "early_reject"):
+        ok = good[pol] > 0
+        out[pol]["median_goodput_ratio_scorpio_over_this"] = (
+            float(np.median(good["scorpio"][ok] / good[pol][ok])) if ok.any() else None)
+    return out
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -510,6 +549,8 @@ def run_ours(args) -> None:
             line["config4_noisy_predictor_sweep"] = config4_sweep(dev)
         if not args.no_report and world == 1:
             line["run_report_on_device"] = report_bench(grid, dev)
+        if not args.no_baselines and world == 1:
+            line["baseline_policies"] = baselines_bench(grid, dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -535,6 +576,8 @@ def main() -> None:
     ap.add_argument("--no-plan", action="store_true", help="skip the config-2 plan microbench")
     ap.add_argument("--no-config4", action="store_true",
                     help="skip the config-4 sweep (16k sims, noisy predictor in the loop)")
+    ap.add_argument("--no-baselines", action="store_true",
+                    help="skip the baseline-policy sweeps (greedy / sjf / early_reject)")
     ap.add_argument("--no-report", action="store_true",
                     help="skip the device RunReport timing (config-3 sweep with outcomes)")
     args = ap.parse_args()
