@@ -224,6 +224,50 @@ __device__ void run_sim(Sim& s, const KArgs& a, bool has_out, int sim_index, int
 
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
 
+    // ---- quiet decode-all steps (baselines, admit-all ablation): nothing can be
+    // admitted or rejected (no waiting request; or a full batch cap and no TTFT
+    // walk) and every running entry decodes each step, so until the next
+    // arrival, the horizon or the step before the first retirement only the
+    // clock and the digest move; per-entry counters are settled once after.
+    if (!(scorpio && tpot_guard) && !logging && R > 0 &&
+        (W == 0 || (!scorpio && s.policy != SL_POLICY_EARLY_REJECT && R >= s.cap))) {
+      int minrem = 1 << 30;
+      int64_t bl = 0;
+      uint32_t bh = 0;
+      for (int j = lane; j < R; j += 32) {
+        const RRec& r = s.rr[j];
+        minrem = min(minrem, r.rem);
+        bl += r.cur_len;
+        bh += s.rh[j];
+      }
+      minrem = __reduce_min_sync(SL_FULL, minrem);
+      bl = warp_sum_i64(bl);
+      bh = __reduce_add_sync(SL_FULL, bh);
+      int k = 0;
+      while (k + 1 < minrem && next_t > now && !(has_h && now >= s.horizon)) {
+        const double decode_s = itl(C, R, div_small((double)bl, R));
+        const double end = fadd_(fadd_(now, 0.0), decode_s);  // prefill sum of no admission
+        if (lane == 0)
+          acc.dig += digest_item((uint64_t)step, 2, (uint32_t)R, bh) +
+                     digest_item((uint64_t)step, 3, 0, (uint64_t)__double_as_longlong(end));
+        n_plans++;
+        req_steps += W + R;
+        bl += R;
+        now = end;
+        step++;
+        ++k;
+      }
+      if (k > 0) {
+        for (int j = lane; j < R; j += 32) {
+          RRec& r = s.rr[j];
+          r.cur_len += k;
+          r.rem -= k;
+        }
+        __syncwarp();
+        continue;  // arrivals / horizon / the retiring step through the general step
+      }
+    }
+
     // ---- plan (policy.plan)
     n_plans++;
     req_steps += W + R;
