@@ -677,6 +677,9 @@ constexpr int kFastWarps = 4;
 #ifndef SL_SIM_IN_SMEM
 #define SL_SIM_IN_SMEM 1
 #endif
+#ifndef SL_BASELINE_TO_GENERAL
+#define SL_BASELINE_TO_GENERAL 1
+#endif
 #ifndef SL_HOT_MIN_BLOCKS
 #define SL_HOT_MIN_BLOCKS 4  // 16 warps/SM for the hot kernel (<= 128 registers)
 #endif
@@ -727,7 +730,11 @@ __global__ void __launch_bounds__(32 * kFastWarps, HOT ? SL_HOT_MIN_BLOCKS : 1) 
     const sl_sim& sp = a.sims[si];
     const bool hot = hot_eligible(sp);
     if (HOT ? !hot : (hot && !a.has_log)) continue;  // the other fast kernel's sim
-    if ((sp.flags & SL_FLAG_GENERAL_ONLY) || sp.credit_wide) {  // 128-bit credits: general
+    // 128-bit credits, or a baseline whose batch cap exceeds the register
+    // slots (its running set soon outgrows them): the general kernel from the start
+    if ((sp.flags & SL_FLAG_GENERAL_ONLY) || sp.credit_wide ||
+        (!HOT && SL_BASELINE_TO_GENERAL && sp.policy != SL_POLICY_SCORPIO &&
+         sp.max_batch_size > kRunCap)) {
       if (lane == 0) a.results[si].status = SL_SIM_CAPACITY;
       continue;
     }
