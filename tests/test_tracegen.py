@@ -41,3 +41,18 @@ def test_generate_objects_match_arrays():
     assert len(objs) == len(arr["arrival"])
     assert [q.arrival_time for q in objs] == arr["arrival"].tolist()
     assert [q.true_output_len for q in objs] == arr["true_out"].tolist()
+
+
+def test_non_lognormal_lengths_use_the_draw_loop():
+    """Uniform / empirical length distributions are not on the native path: the
+    arrays come from the Python draw loop and still equal generate()."""
+    spec = W.WorkloadSpec(qps=6.0, duration=60.0, seed=5,
+                          prompt_len_dist=W.UniformDist(10, 500),
+                          output_len_dist=W.EmpiricalDist((3, 7, 50, 200)),
+                          category_weights=(1.0,) * 6)
+    assert W._draw_native(spec, None) is None
+    objs = W.generate(spec)
+    arr = W.generate_arrays(spec)
+    assert [q.prompt_len for q in objs] == arr["prompt_len"].tolist()
+    assert [q.true_output_len for q in objs] == arr["true_out"].tolist()
+    assert [q.arrival_time for q in objs] == arr["arrival"].tolist()
