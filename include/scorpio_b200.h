@@ -145,11 +145,14 @@ typedef struct {
 /* Per-sim RunReport reductions (report.summarize, report.py:71-127) computed on
  * the device from the outcomes an sl_run_batch wrote (cells with outcomes):
  * nearest-rank p50/p90/p99 of TTFT (s) and TPOT (ms) over completed requests
- * (NaN when none; n_completed = -1 for cells without outcomes). */
+ * (NaN when none; n_completed = -1 for cells without outcomes).
+ * status_first[k]: index of the first request whose status code is k (total
+ * when none) -- summarize() builds status_counts in first-occurrence order. */
 typedef struct {
   double ttft_p[3];
   double tpot_ms_p[3];
   int64_t n_completed;
+  int64_t status_first[4];
 } sl_report_row;
 
 /* Optional decision log (EventLog.steps, simengine.py:80-137), one row per
@@ -232,6 +235,9 @@ int sl_selftest_div_small(const double* a, const int32_t* b, double* out, int64_
 #define SL_PLAN_GUARD_ONLY 64 /* flag: ttft_guard alone (no admission, sched_scorpio.py:183) */
 #define SL_PLAN_FCFS_WALK 128 /* flag: TTFT walk over the unsorted FCFS queue
                                  (early_reject, sched_baselines.py:89-106) */
+#define SL_PLAN_EXACT_WALK 256 /* flag: some prefill_s < 0 (legal when alpha_p < 0,
+                                  costmodel.py:59-65): prefixes may shrink, so the
+                                  walk runs without its monotone shortcuts */
 
 typedef struct {
   int32_t n_segments;
@@ -324,7 +330,8 @@ int sl_predict_batch(const int64_t* id, const int32_t* true_out, int64_t n,
 
 /* ABI self-description: writes sizeof(sl_sim), sizeof(sl_result),
  * sizeof(sl_traces), sizeof(sl_outcomes), sizeof(sl_log), sizeof(sl_cost),
- * sizeof(sl_predictor) into out[0..6] (n >= 7).  Lets bindings verify their struct mirrors. */
+ * sizeof(sl_predictor) into out[0..6] (n >= 7), and sizeof(sl_report_row) into
+ * out[7] when n >= 8.  Lets bindings verify their struct mirrors. */
 int sl_abi_layout(int64_t* out, int32_t n);
 
 /* Device properties used for grid sizing. */

@@ -63,10 +63,10 @@ RESULT_DTYPE = np.dtype({
 
 REPORT_DTYPE = np.dtype({  # sl_report_row
     "names": ["ttft_p50", "ttft_p90", "ttft_p99", "tpot_ms_p50", "tpot_ms_p90", "tpot_ms_p99",
-              "n_completed"],
-    "formats": ["<f8"] * 6 + ["<i8"],
-    "offsets": [8 * k for k in range(7)],
-    "itemsize": 56,
+              "n_completed", "status_first"],
+    "formats": ["<f8"] * 6 + ["<i8", ("<i8", (4,))],
+    "offsets": [8 * k for k in range(8)],
+    "itemsize": 88,
 })
 
 
@@ -121,6 +121,7 @@ class SlPlanOut(C.Structure):
 PLAN_WAITING, PLAN_REJECTED_TTFT, PLAN_REJECTED_ADMISSION, PLAN_ADMITTED = 0, 1, 2, 3
 PLAN_GUARD_ONLY = 64
 PLAN_FCFS_WALK = 128
+PLAN_EXACT_WALK = 256
 
 
 class SlPredictor(C.Structure):
@@ -212,11 +213,11 @@ _OPTIONAL_SIGS: dict = {}
 
 
 def _check_layout(L) -> None:
-    out = (C.c_int64 * 7)()
-    if L.sl_abi_layout(out, 7) != 0:
+    out = (C.c_int64 * 8)()
+    if L.sl_abi_layout(out, 8) != 0:
         raise NativeUnavailable("sl_abi_layout failed")
     want = (SIM_DTYPE.itemsize, RESULT_DTYPE.itemsize, C.sizeof(SlTraces), C.sizeof(SlOutcomes),
-            C.sizeof(SlLog), 8 * len(COST_FIELDS), C.sizeof(SlPredictor))
+            C.sizeof(SlLog), 8 * len(COST_FIELDS), C.sizeof(SlPredictor), REPORT_DTYPE.itemsize)
     if tuple(out) != want:
         raise NativeUnavailable(f"ABI layout mismatch: library {tuple(out)} vs binding {want}")
 

@@ -118,48 +118,108 @@ class Cell:
     rate_factor: float = 1.0
 
 
+_MIN_NORMAL = 2.2250738585072014e-308
+
+
+def credit_params_many(uniq_tpot: np.ndarray, scales: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """(E, wide) of the fixed-point credits for many cells sharing one trace
+    (vectorised ``sl_credit_params``): E = min frexp exponent of the scaled TPOT
+    SLOs - 53; wide when 2 * S_max needs more than 64 bits."""
+    n = len(scales)
+    if len(uniq_tpot) == 0:
+        return np.zeros(n, np.int32), np.zeros(n, np.int32)
+    prod = uniq_tpot[None, :] * scales[:, None]  # one IEEE multiply each, as on device
+    if not (np.isfinite(prod).all() and (prod >= _MIN_NORMAL).all()):
+        raise ValueError("TPOT SLOs must be positive normal doubles within the credit range")
+    ex = np.frexp(prod)[1]
+    emin, emax = ex.min(axis=1), ex.max(axis=1)
+    E = emin - 53
+    span = emax - emin
+    if (E < -1022).any() or (53 + span + 1 > 128).any():
+        raise ValueError("TPOT SLOs must be positive normal doubles within the credit range")
+    return E.astype(np.int32), (53 + span + 1 > 64).astype(np.int32)
+
+
+def _config_row(cfg: CellConfig) -> tuple:
+    """Validated (policy code, flags, cap, horizon, 9 cost coefficients) of one config."""
+    if cfg.policy not in N.POLICY:
+        raise ValueError(f"unknown policy {cfg.policy!r}")
+    a, b, g, d, e = (float(x) for x in cfg.itl)
+    if e < 1.0:
+        raise ValueError("epsilon must be >= 1.0")
+    phi, th, ap, bp = (float(x) for x in cfg.prefill)
+    if phi <= 0 or th < 0 or ap * th + bp < 0:
+        raise ValueError("invalid PrefillParams")
+    if cfg.max_batch_size < 1:
+        raise ValueError("max_batch_size must be >= 1")
+    return (N.POLICY[cfg.policy], cfg.flags(), int(cfg.max_batch_size),
+            float(cfg.horizon) if cfg.horizon is not None else 0.0, a, b, g, d, e, phi, th, ap, bp)
+
+
 def pack_cells(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = False,
                log_cells: list[int] | None = None) -> np.ndarray:
-    """Build the sl_sim table (host); workspace/outcome offsets by prefix sum."""
-    sims = np.zeros(len(cells), N.SIM_DTYPE)
-    uniq = [np.unique(t.tpot_slo) for t in traces]
-    # the fast kernel sums up to 64 current lengths in 32 bits
-    huge = [bool(len(t) and int((t.prompt_len.astype(np.int64) + t.true_out).max()) >= 1 << 26)
-            for t in traces]
-    ws = 0
-    log_rows = {c: r for r, c in enumerate(log_cells or [])}
+    """Build the sl_sim table (host), column-wise: per-config rows are validated
+    once per distinct config object, credit exponents per trace for all its
+    cells at once, workspace/outcome offsets by prefix sum."""
+    n = len(cells)
+    sims = np.zeros(n, N.SIM_DTYPE)
+    if n == 0:
+        return sims
+    tr_idx = np.fromiter((c.trace for c in cells), np.int64, n)
+    scale = np.fromiter((c.slo_scale for c in cells), np.float64, n)
+    factor = np.fromiter((c.rate_factor for c in cells), np.float64, n)
+    if not ((scale > 0).all() and (factor > 0).all()):
+        raise ValueError("slo_scale and rate_factor must be positive")
+    rows: dict[int, tuple] = {}
+    keys = np.empty(n, np.int64)
+    table = []
     for k, c in enumerate(cells):
-        t = traces[c.trace]
-        cfg = c.config
-        if cfg.policy not in N.POLICY:
-            raise ValueError(f"unknown policy {cfg.policy!r}")
-        if not c.slo_scale > 0 or not c.rate_factor > 0:
-            raise ValueError("slo_scale and rate_factor must be positive")
-        a, b, g, d, e = cfg.itl
-        if e < 1.0:
-            raise ValueError("epsilon must be >= 1.0")
-        phi, th, ap, bp = cfg.prefill
-        if phi <= 0 or th < 0 or ap * th + bp < 0:
-            raise ValueError("invalid PrefillParams")
-        if cfg.max_batch_size < 1:
-            raise ValueError("max_batch_size must be >= 1")
-        E, wide = N.credit_params(uniq[c.trace], c.slo_scale)
-        s = sims[k]
-        s["trace"] = c.trace
-        s["policy"] = N.POLICY[cfg.policy]
-        s["flags"] = cfg.flags() | (N.FLAG_GENERAL_ONLY if huge[c.trace] else 0)
-        s["max_batch_size"] = cfg.max_batch_size
-        s["slo_scale"] = c.slo_scale
-        s["rate_factor"] = c.rate_factor
-        s["horizon"] = cfg.horizon if cfg.horizon is not None else 0.0
-        s["credit_exp"] = E
-        s["credit_wide"] = wide
-        s["ws_offset"] = ws
-        s["out_offset"] = ws if outcomes else -1
-        s["log_slot"] = log_rows.get(k, -1)
-        for name, v in zip(N.COST_FIELDS, (a, b, g, d, e, phi, th, ap, bp)):
-            s[name] = v
-        ws += len(t)
+        key = id(c.config)
+        r = rows.get(key)
+        if r is None:
+            r = rows[key] = (len(table), c.config)
+            table.append(_config_row(c.config))
+        keys[k] = r[0]
+    cols = {name: np.array([row[j] for row in table])[keys]
+            for j, name in enumerate(("policy", "flags", "max_batch_size", "horizon")
+                                     + N.COST_FIELDS)}
+    lens = np.array([len(t) for t in traces], np.int64)
+    flags = cols["flags"].astype(np.int32)
+    E = np.zeros(n, np.int32)
+    wide = np.zeros(n, np.int32)
+    for t in np.unique(tr_idx):
+        sel = np.nonzero(tr_idx == t)[0]
+        tt = traces[int(t)]
+        E[sel], wide[sel] = credit_params_many(np.unique(tt.tpot_slo), scale[sel])
+        if len(tt):
+            big = int(tt.prompt_len.max())
+            # the fast kernel sums up to 64 current lengths in 32 bits
+            if int((tt.prompt_len.astype(np.int64) + tt.true_out).max()) >= 1 << 26:
+                flags[sel] |= N.FLAG_GENERAL_ONLY
+            # a negative prefill_time (alpha_p < 0 past -beta_p/alpha_p) breaks the
+            # fast kernel's monotone-prefix walk shortcuts: exact general kernel
+            ap, bp, th = cols["alpha_p"][sel], cols["beta_p"][sel], cols["theta"][sel]
+            neg = (ap < 0) & (big > th) & (ap * float(big) + bp < 0)
+            flags[sel[neg]] |= N.FLAG_GENERAL_ONLY
+    ws = np.zeros(n, np.int64)
+    np.cumsum(lens[tr_idx][:-1], out=ws[1:])
+    log_slot = np.full(n, -1, np.int32)
+    if log_cells:
+        log_slot[np.asarray(log_cells, np.int64)] = np.arange(len(log_cells), dtype=np.int32)
+    sims["trace"] = tr_idx
+    sims["policy"] = cols["policy"]
+    sims["flags"] = flags
+    sims["max_batch_size"] = cols["max_batch_size"]
+    sims["slo_scale"] = scale
+    sims["rate_factor"] = factor
+    sims["horizon"] = cols["horizon"]
+    sims["credit_exp"] = E
+    sims["credit_wide"] = wide
+    sims["ws_offset"] = ws
+    sims["out_offset"] = ws if outcomes else -1
+    sims["log_slot"] = log_slot
+    for name in N.COST_FIELDS:
+        sims[name] = cols[name].astype(np.float64)
     return sims
 
 
@@ -266,22 +326,31 @@ class BatchEngine:
     def results_device(self):
         return self._res
 
-    def report(self, traces: list[TraceArrays] | None = None, n_categories: int = 8):
+    def report(self, traces: list[TraceArrays] | None = None, n_categories: int | None = None):
         """RunReport reductions per cell on the device (sl_report_batch, one launch):
         returns (rows, cat_counts) -- rows: REPORT_DTYPE (nearest-rank p50/p90/p99
-        of TTFT in s and TPOT in ms over completed requests); cat_counts:
-        [n_sims, n_categories, 2] (total, compliant) per request category, the
-        categories taken from `traces` (TraceArrays.category), else all 0."""
+        of TTFT in s and TPOT in ms over completed requests, first index of each
+        status); cat_counts: [n_sims, n_categories, 2] (total, compliant) per
+        request category, the categories taken from `traces`
+        (TraceArrays.category), else all 0.  `n_categories` defaults to
+        max(category) + 1; a category outside [0, n_categories) or above 127
+        raises (nothing is dropped silently)."""
         if not self.has_outcomes:
             raise RuntimeError("engine built without outcomes")
         torch = self.torch
         cat = None
+        hi = 0
         if traces is not None:
             c = np.concatenate([np.asarray(t.category) for t in traces]) if traces else \
                 np.zeros(0, np.int8)
-            if len(c) and (c.min() < -128 or c.max() > 127):
-                raise ValueError("categories must fit in int8")
+            if len(c) and (c.min() < 0 or c.max() > 127):
+                raise ValueError("request categories must lie in [0, 127] for the device report")
+            hi = int(c.max()) + 1 if len(c) else 0
             cat = torch.from_numpy(np.ascontiguousarray(c, np.int8)).to(self.device)
+        if n_categories is None:
+            n_categories = max(hi, 1)
+        elif hi > n_categories:
+            raise ValueError(f"category {hi - 1} outside [0, {n_categories})")
         rows = torch.empty(max(self.n_sims, 1) * N.REPORT_DTYPE.itemsize, dtype=torch.uint8,
                            device=self.device)
         counts = torch.zeros(max(self.n_sims * n_categories * 2, 1), dtype=torch.int64,

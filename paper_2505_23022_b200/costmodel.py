@@ -29,7 +29,7 @@ class ItlParams:
             raise ValueError("epsilon must be >= 1.0")
 
     def as_tuple(self) -> tuple[float, float, float, float, float]:
-        return (self.alpha, self.beta, self.gamma, self.delta, self.epsilon)
+        return itl_coeffs(self)
 
 
 @dataclass(frozen=True)
@@ -50,7 +50,18 @@ class PrefillParams:
             raise ValueError("linear regime must be non-negative at theta")
 
     def as_tuple(self) -> tuple[float, float, float, float]:
-        return (self.phi, self.theta, self.alpha_p, self.beta_p)
+        return prefill_coeffs(self)
+
+
+def itl_coeffs(p) -> tuple[float, float, float, float, float]:
+    """(alpha, beta, gamma, delta, epsilon) of any ItlParams-shaped object
+    (this package's or the reference's, costmodel.py:31-47)."""
+    return (float(p.alpha), float(p.beta), float(p.gamma), float(p.delta), float(p.epsilon))
+
+
+def prefill_coeffs(p) -> tuple[float, float, float, float]:
+    """(phi, theta, alpha_p, beta_p) of any PrefillParams-shaped object (costmodel.py:50-65)."""
+    return (float(p.phi), float(p.theta), float(p.alpha_p), float(p.beta_p))
 
 
 def itl(params: ItlParams, batch_size: float, avg_len: float) -> float:

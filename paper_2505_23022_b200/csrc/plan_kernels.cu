@@ -222,6 +222,9 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   const bool r_only = cfg.flags & SL_FLAG_R_ONLY;
   const bool guard_only = cfg.flags & SL_PLAN_GUARD_ONLY;
   const bool walk = ttft_guard || (cfg.flags & SL_PLAN_FCFS_WALK);
+  // negative prefills: no certified pass, no outright rejection (both assume
+  // the prefix only grows); the speculative chain + serial pass stays exact
+  const bool exact = cfg.flags & SL_PLAN_EXACT_WALK;
   const int64_t wb = st.w_begin[seg], rb = st.r_begin[seg];
   const int W = (int)(st.w_begin[seg + 1] - wb);
   const int R = (int)(st.r_begin[seg + 1] - rb);
@@ -237,7 +240,7 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   // est_j <= fl(fl(e_j + U_j) + pf_j); if that passes for every item nothing is
   // rejected and the exact chain is not needed.
   bool certified = !walk;
-  if (walk && W < (1 << 20)) {
+  if (walk && !exact && W < (1 << 20)) {
     const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
     double U = 0.0;
     bool all_ok = true;
@@ -299,7 +302,7 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
         // items failing at the chunk's incoming prefix fail at any later one
         // (prefixes only grow, est is monotone in them): rejected outright,
         // and the speculative chain runs over the remaining items only
-        rejm = __ballot_sync(SL_FULL, valid && fadd_(fadd_(e, prefix), pf) > tt);
+        rejm = exact ? 0u : __ballot_sync(SL_FULL, valid && fadd_(fadd_(e, prefix), pf) > tt);
         const unsigned live = (cnt == 32 ? ~0u : (1u << cnt) - 1u) & ~rejm;
         if (live) {
           // speculative chain over the undecided items (assumed kept), tested

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kThreads) report_kernel(const sl_traces tr, co
   __shared__ unsigned hist[kRanks * 256];
   __shared__ unsigned long long ncomp;
   __shared__ uint64_t sel[kRanks];
+  __shared__ unsigned long long sfirst[4];
   extern __shared__ unsigned long long cat_sm[];  // [n_cat][2]
   const int si = blockIdx.x;
   const sl_sim& sp = sims[si];
@@ -92,11 +93,16 @@ __global__ void __launch_bounds__(kThreads) report_kernel(const sl_traces tr, co
   const double* ttft = oc.ttft + sp.out_offset;
   const double* tpot = oc.tpot + sp.out_offset;
   if (threadIdx.x == 0) ncomp = 0;
+  if (threadIdx.x < 4) sfirst[threadIdx.x] = (unsigned long long)n;
   for (int c = threadIdx.x; c < 2 * n_cat; c += blockDim.x) cat_sm[c] = 0;
   __syncthreads();
   unsigned long long mine = 0;
+  unsigned long long first[4] = {(unsigned long long)n, (unsigned long long)n,
+                                 (unsigned long long)n, (unsigned long long)n};
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    mine += status[i] == SL_COMPLETED;
+    const int sc = status[i];
+    mine += sc == SL_COMPLETED;
+    if (sc >= 0 && sc < 4 && first[sc] == (unsigned long long)n) first[sc] = (unsigned long long)i;
     const int c = category ? category[b + i] : 0;
     if (c >= 0 && c < n_cat) {
       atomicAdd(&cat_sm[2 * c], 1ull);
@@ -104,6 +110,9 @@ __global__ void __launch_bounds__(kThreads) report_kernel(const sl_traces tr, co
     }
   }
   atomicAdd(&ncomp, mine);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (first[k] < (unsigned long long)n) atomicMin(&sfirst[k], first[k]);
   __syncthreads();
   const int64_t nc = (int64_t)ncomp;
   int64_t rk[kRanks];
@@ -123,6 +132,7 @@ __global__ void __launch_bounds__(kThreads) report_kernel(const sl_traces tr, co
     row->tpot_ms_p[threadIdx.x] =
         nc > 0 ? fmul_(__longlong_as_double((long long)sel[threadIdx.x]), 1000.0) : qnan;
   if (threadIdx.x == 0) row->n_completed = nc;
+  if (threadIdx.x < 4) row->status_first[threadIdx.x] = (int64_t)sfirst[threadIdx.x];
   for (int c = threadIdx.x; c < 2 * n_cat; c += blockDim.x)
     cat_counts[(int64_t)si * 2 * n_cat + c] = (int64_t)cat_sm[c];
 }

@@ -99,31 +99,56 @@ struct KArgs {
   int has_log;
 };
 
+// Pointer known to address global memory.  The hot kernel keeps its per-sim
+// view in shared memory, so nvcc cannot infer the address space of pointers it
+// reloads from there and would emit generic LD/ST; the assumption restores
+// LDG/STG on every access.
+template <class T>
+struct gptr {
+  T* p;
+  __device__ __forceinline__ T* get() const {
+    T* q = p;
+    __builtin_assume(__isGlobal(q));
+    return q;
+  }
+  __device__ __forceinline__ gptr& operator=(T* q) {
+    p = q;
+    return *this;
+  }
+  __device__ __forceinline__ gptr& operator+=(int64_t k) {
+    p += k;
+    return *this;
+  }
+  __device__ __forceinline__ T& operator[](int64_t i) const { return get()[i]; }
+  __device__ __forceinline__ T* operator+(int64_t i) const { return get() + i; }
+  __device__ __forceinline__ operator T*() const { return get(); }
+};
+
 // Per-sim view, warp-uniform.
 struct Sim {
   // trace
-  const double* arrival;
-  const double* ttft_b;
-  const double* tpot_b;
-  const int32_t* prompt;
-  const int32_t* true_out;
-  const int32_t* predicted;
-  const int64_t* id;
+  gptr<const double> arrival;
+  gptr<const double> ttft_b;
+  gptr<const double> tpot_b;
+  gptr<const int32_t> prompt;
+  gptr<const int32_t> true_out;
+  gptr<const int32_t> predicted;
+  gptr<const int64_t> id;
   int64_t n;
   // params
   sl_cost cost;
   double scale, factor, horizon, pow2E;
   int policy, flags, cap, E;
   // workspace slices
-  int32_t* wl;
-  int32_t* rl;
-  uint32_t* rh;
-  WRec* wr;
-  RRec* rr;
-  uint64_t* wShi;
-  uint64_t* rNhi;
-  uint64_t* rShi;
-  double* first_emit;
+  gptr<int32_t> wl;
+  gptr<int32_t> rl;
+  gptr<uint32_t> rh;
+  gptr<WRec> wr;
+  gptr<RRec> rr;
+  gptr<uint64_t> wShi;
+  gptr<uint64_t> rNhi;
+  gptr<uint64_t> rShi;
+  gptr<double> first_emit;
   // outputs
   int64_t out_off;
   int64_t log_row;

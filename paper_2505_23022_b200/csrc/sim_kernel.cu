@@ -822,6 +822,7 @@ int sl_phase_prof_read(uint64_t* out, int32_t n_sims) {
 
 int sl_abi_layout(int64_t* out, int32_t n) {
   if (!out || n < 7) return SL_ERR_ARG;
+  if (n >= 8) out[7] = sizeof(sl_report_row);
   out[0] = sizeof(sl_sim);
   out[1] = sizeof(sl_result);
   out[2] = sizeof(sl_traces);

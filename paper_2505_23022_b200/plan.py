@@ -53,9 +53,13 @@ def _dyadic_exp(x: Fraction) -> int:
     return e
 
 
-def segment_exponent(tpots: list[float], credits: list[tuple[Fraction, float]]) -> int:
+def segment_exponent(tpots: list[float], credits: list[tuple[Fraction, float]],
+                     need_credits: bool = True) -> int:
     """Fixed-point exponent E for one state: every SLO and every credit*slo
-    must be an integer multiple of 2^E."""
+    must be an integer multiple of 2^E.  Without a credit phase (ttft_guard,
+    admit, the early-reject walk) the span limit does not apply."""
+    if not need_credits:
+        return 0
     E = 1 << 20
     for t in tpots:
         m, e = math.frexp(t)
@@ -75,12 +79,15 @@ class PlanBatch:
     """Device SoA for a batch of SchedulerStates (segments)."""
 
     def __init__(self, states: list[SchedulerState] | None = None, device=None,
-                 arrays: dict | None = None):
+                 arrays: dict | None = None, need_credits: bool = True):
         torch = N.require_cuda()
         self.torch = torch
         self.dev = torch.device(device if device is not None else "cuda")
         self.states = states
-        host = arrays if arrays is not None else self._pack(states)
+        host = arrays if arrays is not None else self._pack(states, need_credits)
+        # negative prefills (alpha_p < 0 past -beta_p/alpha_p) disable the walk's
+        # monotone shortcuts in the kernels
+        self.exact_walk = bool(len(host["w_prefill"]) and (host["w_prefill"] < 0).any())
         S = len(host["now"])
         self.w_begin = host["w_begin"]
         self.r_begin = host["r_begin"]
@@ -121,7 +128,7 @@ class PlanBatch:
             "r_batch", "r_pos", "seg_counts", "seg_min_fixed", "seg_vbs", "seg_min_slo")])
 
     @staticmethod
-    def _pack(states: list[SchedulerState]) -> dict[str, np.ndarray]:
+    def _pack(states: list[SchedulerState], need_credits: bool = True) -> dict[str, np.ndarray]:
         S = len(states)
         w_begin = np.zeros(S + 1, np.int64)
         r_begin = np.zeros(S + 1, np.int64)
@@ -131,10 +138,11 @@ class PlanBatch:
         ents = [e for s in states for e in s.running]
         E = np.array([segment_exponent(
             [w.request.tpot_slo for w in s.waiting] + [e.request.tpot_slo for e in s.running],
-            [(e.credit, e.request.tpot_slo) for e in s.running]) for s in states], np.int32)
+            [(e.credit, e.request.tpot_slo) for e in s.running], need_credits)
+            for s in states], np.int32)
         credit = np.zeros(len(ents), np.uint64)
         k = 0
-        for si, s in enumerate(states):
+        for si, s in enumerate(states if need_credits else []):
             scale = Fraction(2) ** (-int(E[si]))
             for e in s.running:
                 n = Fraction(e.credit) * Fraction(e.request.tpot_slo) * scale
@@ -171,6 +179,8 @@ class PlanBatch:
     def _cfg(self, flags: int, itl, prefill) -> N.SlPlanConfig:
         a, b, g, d, e = itl
         phi, th, ap, bp = prefill
+        if self.exact_walk:
+            flags |= N.PLAN_EXACT_WALK
         return N.SlPlanConfig(flags, 0, N.SlCost(a, b, g, d, e, phi, th, ap, bp))
 
     def _stream(self):

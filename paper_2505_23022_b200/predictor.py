@@ -102,37 +102,52 @@ class LengthPredictor:
     def predict(self, req: Request) -> int:
         if self.mode == ORACLE:
             return req.true_output_len
-        return int(self.predict_batch(np.array([req.id]), np.array([req.true_output_len]))[0])
+        return int(predict_many(self, np.array([req.id]), np.array([req.true_output_len]))[0])
 
     def predict_batch(self, ids: np.ndarray, true_out: np.ndarray, device=None,
                       return_clamps: bool = False):
         """Predicted lengths for many requests in one device launch (host arrays
         in, host array out; see predict_device for device tensors)."""
-        torch = N.require_cuda()
-        dev = torch.device(device if device is not None else "cuda")
-        ids_t = torch.from_numpy(np.ascontiguousarray(ids, np.int64)).to(dev)
-        tout_t = torch.from_numpy(np.ascontiguousarray(true_out, np.int32)).to(dev)
-        out, clamps = self.predict_device(ids_t, tout_t)
-        res = out.cpu().numpy()
-        return (res, int(clamps.item())) if return_clamps else res
+        return predict_many(self, ids, true_out, device, return_clamps)
 
     def predict_device(self, ids_t, true_out_t, stream=None):
         """Device tensors in (int64 ids, int32 lengths), device tensor out."""
-        torch = N.require_cuda()
-        if len(ids_t) and int(true_out_t.min().item()) < 1:
-            raise ValueError("length must be >= 1")
-        if self.rng_seed < 0 or self.rng_seed >= 1 << 64 or (len(ids_t) and int(ids_t.min().item()) < 0):
-            raise ValueError("seed and request ids must be non-negative 64-bit integers")
-        dev = ids_t.device
-        bounds = torch.tensor(self.bucketing.boundaries, dtype=torch.float64, device=dev)
-        out = torch.empty(len(ids_t), dtype=torch.int32, device=dev)
-        clamps = torch.zeros(1, dtype=torch.int64, device=dev)
-        p = N.SlPredictor(N.PREDICT_ORACLE if self.mode == ORACLE else N.PREDICT_NOISY_BUCKET,
-                          self.bucketing.num_buckets, bounds.data_ptr(), float(self.error_prob),
-                          int(self.error_spread), 0, int(self.rng_seed))
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
-        rc = N.lib().sl_predict_batch(ids_t.data_ptr(), true_out_t.data_ptr(), len(ids_t),
-                                      C.byref(p), out.data_ptr(), clamps.data_ptr(), s.cuda_stream)
-        if rc != 0:
-            raise RuntimeError(f"sl_predict_batch failed with code {rc}")
-        return out, clamps
+        return predict_device(self, ids_t, true_out_t, stream)
+
+
+def predict_many(predictor, ids: np.ndarray, true_out: np.ndarray, device=None,
+                 return_clamps: bool = False):
+    """``predictor.predict`` for many requests in one launch.  ``predictor`` is
+    any LengthPredictor-shaped object (this package's or the reference's,
+    predictor.py:93-126): only its fields are read."""
+    torch = N.require_cuda()
+    dev = torch.device(device if device is not None else "cuda")
+    ids_t = torch.from_numpy(np.ascontiguousarray(ids, np.int64)).to(dev)
+    tout_t = torch.from_numpy(np.ascontiguousarray(true_out, np.int32)).to(dev)
+    out, clamps = predict_device(predictor, ids_t, tout_t)
+    res = out.cpu().numpy()
+    return (res, int(clamps.item())) if return_clamps else res
+
+
+def predict_device(predictor, ids_t, true_out_t, stream=None):
+    """Device tensors in (int64 ids, int32 lengths), device tensor out."""
+    torch = N.require_cuda()
+    p_ = predictor
+    if len(ids_t) and int(true_out_t.min().item()) < 1:
+        raise ValueError("length must be >= 1")
+    if p_.rng_seed < 0 or p_.rng_seed >= 1 << 64 or (len(ids_t) and int(ids_t.min().item()) < 0):
+        raise ValueError("seed and request ids must be non-negative 64-bit integers")
+    dev = ids_t.device
+    bk = p_.bucketing
+    bounds = torch.tensor([float(b) for b in bk.boundaries], dtype=torch.float64, device=dev)
+    out = torch.empty(len(ids_t), dtype=torch.int32, device=dev)
+    clamps = torch.zeros(1, dtype=torch.int64, device=dev)
+    p = N.SlPredictor(N.PREDICT_ORACLE if p_.mode == ORACLE else N.PREDICT_NOISY_BUCKET,
+                      int(bk.num_buckets), bounds.data_ptr(), float(p_.error_prob),
+                      int(p_.error_spread), 0, int(p_.rng_seed))
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    rc = N.lib().sl_predict_batch(ids_t.data_ptr(), true_out_t.data_ptr(), len(ids_t),
+                                  C.byref(p), out.data_ptr(), clamps.data_ptr(), s.cuda_stream)
+    if rc != 0:
+        raise RuntimeError(f"sl_predict_batch failed with code {rc}")
+    return out, clamps

@@ -14,8 +14,9 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import _native as N
+from ._family import family
 from .core import Request, Status
-from .costmodel import ItlParams, PrefillParams, prefill_time
+from .costmodel import ItlParams, PrefillParams, itl_coeffs, prefill_coeffs, prefill_time
 from .plan import PlanBatch, vbs_batch
 from .predictor import LengthPredictor
 from .schedtypes import AdmissionRecord, RunningEntry, SchedulerState, StepPlan, WaitingItem
@@ -24,8 +25,8 @@ SCORPIO = "scorpio"
 R_PRIME = "r_prime"
 R_ONLY = "r_only"
 
-_STATUS = {N.PLAN_REJECTED_TTFT: Status.REJECTED_TTFT,
-           N.PLAN_REJECTED_ADMISSION: Status.REJECTED_ADMISSION}
+_REJECT_NAME = {N.PLAN_REJECTED_TTFT: "REJECTED_TTFT",
+                N.PLAN_REJECTED_ADMISSION: "REJECTED_ADMISSION"}
 
 
 @dataclass(frozen=True)
@@ -41,10 +42,17 @@ class ScorpioConfig:
             raise ValueError(f"unknown admission_min {self.admission_min!r}")
 
     def flags(self) -> int:
-        f = N.FLAG_TTFT_GUARD if self.ttft_guard else 0
-        f |= N.FLAG_TPOT_GUARD if self.tpot_guard else 0
-        f |= N.FLAG_R_ONLY if self.admission_min == R_ONLY else 0
-        return f
+        return scorpio_flags(self)
+
+
+def scorpio_flags(config) -> int:
+    """Kernel flag word of any ScorpioConfig-shaped object (sched_scorpio.py:43-60)."""
+    if config.admission_min not in (R_PRIME, R_ONLY):
+        raise ValueError(f"unknown admission_min {config.admission_min!r}")
+    f = N.FLAG_TTFT_GUARD if config.ttft_guard else 0
+    f |= N.FLAG_TPOT_GUARD if config.tpot_guard else 0
+    f |= N.FLAG_R_ONLY if config.admission_min == R_ONLY else 0
+    return f
 
 
 def trp(tpot_slo: float, running_min_slo: float) -> float:
@@ -64,26 +72,30 @@ def vbs(running: list[RunningEntry], min_slo: float) -> float:
 
 
 def _apply_plan(state: SchedulerState, r, plan: StepPlan | None, records: bool) -> None:
-    """Apply one segment's device decisions to the reference-shaped objects."""
+    """Apply one segment's device decisions to the caller's objects (this
+    package's or the reference's classes, whichever ``state`` belongs to)."""
+    fam = family(state)
     items = state.waiting
     running_before = list(state.running)
     # rejected, in plan order (TTFT walk first, then the admission scan)
     rej = sorted((int(r.w_pos[i]), i) for i in range(len(items))
-                 if int(r.w_status[i]) in _STATUS)
+                 if int(r.w_status[i]) in _REJECT_NAME)
     admitted = []
     for k in r.adm_order:
         it = items[int(k)]
-        e = RunningEntry(request=it.request, predicted_len=it.predicted_len, prefill_s=it.prefill_s)
+        e = fam.RunningEntry(request=it.request, predicted_len=it.predicted_len,
+                             prefill_s=it.prefill_s)
         admitted.append((int(k), e))
     keep = sorted((int(r.w_pos[i]), i) for i in range(len(items))
                   if int(r.w_status[i]) == N.PLAN_WAITING)
     if plan is not None:
-        plan.rejected.extend((items[i], _STATUS[int(r.w_status[i])]) for _, i in rej)
+        plan.rejected.extend((items[i], getattr(fam.Status, _REJECT_NAME[int(r.w_status[i])]))
+                             for _, i in rej)
         if records:
             snap = [(e.request.id, e.request.tpot_slo, e.current_len) for e in running_before]
             for k, e in admitted:
                 v = r.w_rec[k]
-                plan.admissions.append(AdmissionRecord(
+                plan.admissions.append(fam.AdmissionRecord(
                     now=state.now, candidate_id=e.request.id,
                     candidate_tpot_slo=e.request.tpot_slo, candidate_len=e.request.prompt_len,
                     predicted_len=e.predicted_len, running=tuple(snap), vbs=float(v[0]),
@@ -107,16 +119,17 @@ def admit(state: SchedulerState, candidate: Request, predicted_len: int, cost: I
     """Admit ``candidate`` if the projected TPOT allows (:127-158)."""
     if predicted_len < 1:
         raise ValueError("predicted_len must be >= 1")
+    fam = family(state)
     probe = SchedulerState(waiting=[WaitingItem(candidate, predicted_len, prefill_s)],
                            running=state.running, now=state.now)
-    pb = PlanBatch([probe])
+    pb = PlanBatch([probe], need_credits=False)
     flags = N.FLAG_TPOT_GUARD | (N.FLAG_R_ONLY if admission_min == R_ONLY else 0)
-    pb.guard_admit(flags, cost.as_tuple(), (1.0, 0.0, 0.0, 0.0))
+    pb.guard_admit(flags, itl_coeffs(cost), (1.0, 0.0, 0.0, 0.0))
     r = pb.results()[0]
     ok = int(r.w_status[0]) == N.PLAN_ADMITTED
     if ok:
-        state.running.append(RunningEntry(request=candidate, predicted_len=predicted_len,
-                                          prefill_s=prefill_s))
+        state.running.append(fam.RunningEntry(request=candidate, predicted_len=predicted_len,
+                                              prefill_s=prefill_s))
     return ok
 
 
@@ -133,11 +146,11 @@ def select_batch(state: SchedulerState, exclude: set[int] | None = None) -> list
 def ttft_guard(state: SchedulerState, cost: PrefillParams) -> tuple[list[WaitingItem],
                                                                     list[WaitingItem]]:
     """LDF order + drop TTFT-unattainable requests (:183-207)."""
-    pb = PlanBatch([state])
+    pb = PlanBatch([state], need_credits=False)
     if state.waiting:
         pb.sort()
         pb.guard_admit(N.FLAG_TTFT_GUARD | N.PLAN_GUARD_ONLY, (0.0, 0.0, 0.0, 0.0, 1.0),
-                       cost.as_tuple())
+                       prefill_coeffs(cost))
     r = pb.results()[0]
     items = state.waiting
     rejected = [items[i] for _, i in sorted((int(r.w_pos[i]), i) for i in range(len(items))
@@ -153,11 +166,12 @@ def plan_step_batch(states: list[SchedulerState], itl_params: ItlParams,
                     records: bool = True) -> list[StepPlan]:
     """plan_step for many independent states: sort + guard/admit + select kernels,
     one launch each, over all states."""
-    pb = PlanBatch(states)
-    pb.plan(config.flags(), itl_params.as_tuple(), prefill_params.as_tuple())
+    flags = scorpio_flags(config)
+    pb = PlanBatch(states, need_credits=bool(config.tpot_guard))
+    pb.plan(flags, itl_coeffs(itl_params), prefill_coeffs(prefill_params))
     plans = []
     for s, r in zip(states, pb.results()):
-        plan = StepPlan()
+        plan = family(s).StepPlan()
         running_before = list(s.running)
         _apply_plan(s, r, plan, records and config.tpot_guard)
         # fresh entries are not in the kernel's running arrays, so they never batch

@@ -19,10 +19,11 @@ from pathlib import Path
 import numpy as np
 
 from . import _native as N
+from ._family import family
 from .batch import BatchEngine, Cell, CellConfig, TraceArrays
-from .core import STATUS_BY_CODE, Request, RequestOutcome, Status
-from .costmodel import ItlParams, PrefillParams
-from .predictor import LengthPredictor
+from .core import Request, RequestOutcome
+from .costmodel import ItlParams, PrefillParams, itl_coeffs, prefill_coeffs
+from .predictor import ORACLE, LengthPredictor, predict_many
 from .sched_baselines import (EARLY_REJECT, GREEDY, SJF, BaselineConfig, EarlyRejectPolicy,
                               GreedyPolicy, SjfPolicy)
 from .sched_scorpio import SCORPIO, ScorpioConfig, ScorpioPolicy
@@ -49,14 +50,20 @@ class SimConfig:
             raise ValueError("horizon must be positive when finite")
 
     def cell_config(self) -> CellConfig:
-        if self.policy not in (SCORPIO, GREEDY, SJF, EARLY_REJECT):
-            raise ValueError(f"unknown policy {self.policy!r}")
-        return CellConfig(policy=self.policy, itl=self.itl_params.as_tuple(),
-                          prefill=self.prefill_params.as_tuple(),
-                          ttft_guard=self.scorpio.ttft_guard, tpot_guard=self.scorpio.tpot_guard,
-                          admission_min=self.scorpio.admission_min,
-                          max_batch_size=self.baseline.max_batch_size,
-                          prefill_priority=self.baseline.prefill_priority, horizon=self.horizon)
+        return cell_config_of(self)
+
+
+def cell_config_of(config) -> CellConfig:
+    """Flatten any SimConfig-shaped object (this package's or the reference's,
+    simengine.py:46-61) into the device cell config; fields only."""
+    if config.policy not in (SCORPIO, GREEDY, SJF, EARLY_REJECT):
+        raise ValueError(f"unknown policy {config.policy!r}")
+    sc, bl = config.scorpio, config.baseline
+    return CellConfig(policy=config.policy, itl=itl_coeffs(config.itl_params),
+                      prefill=prefill_coeffs(config.prefill_params),
+                      ttft_guard=bool(sc.ttft_guard), tpot_guard=bool(sc.tpot_guard),
+                      admission_min=sc.admission_min, max_batch_size=int(bl.max_batch_size),
+                      prefill_priority=bool(bl.prefill_priority), horizon=config.horizon)
 
 
 def build_policy(config: SimConfig) -> Policy:
@@ -137,10 +144,10 @@ def trace_arrays(trace: list[Request], predictor: LengthPredictor) -> TraceArray
         raise ValueError("trace contains duplicate request ids")
     ids = np.array([r.id for r in trace], np.int64)
     tout = np.array([r.true_output_len for r in trace], np.int32)
-    if predictor.mode == "oracle" or not trace:
+    if predictor.mode == ORACLE or not trace:
         pred = tout.copy()
     else:
-        pred = predictor.predict_batch(ids, tout)
+        pred = predict_many(predictor, ids, tout)
     return TraceArrays(np.array([r.arrival_time for r in trace], np.float64),
                        np.array([r.ttft_slo for r in trace], np.float64),
                        np.array([r.tpot_slo for r in trace], np.float64),
@@ -161,7 +168,7 @@ def run_many(traces: list[list[Request]], configs: list[SimConfig], with_log: bo
     if len(traces) != len(configs):
         raise ValueError("one config per trace")
     arrs = [trace_arrays(t, c.predictor) for t, c in zip(traces, configs)]
-    cells = [Cell(k, c.cell_config()) for k, c in enumerate(configs)]
+    cells = [Cell(k, cell_config_of(c)) for k, c in enumerate(configs)]
     tok = [int(a.true_out.sum()) for a in arrs]
     step_cap = max(tok + [1])
     id_cap = max([len(a) + t for a, t in zip(arrs, tok)] + [1])
@@ -180,11 +187,16 @@ def run_many(traces: list[list[Request]], configs: list[SimConfig], with_log: bo
         r = res[k]
         _raise_status(int(r["status"]))
         o = eng.sim_outcomes(k, out_all)
+        # outcomes / log in the caller's classes (reference Status members keep
+        # the reference summarize()'s identity checks true)
+        fam = family(trace[0] if trace else None, cfg)
+        by_code = (fam.Status.COMPLETED, fam.Status.REJECTED_TTFT,
+                   fam.Status.REJECTED_ADMISSION, fam.Status.INCOMPLETE)
         outcomes = []
         for i, req in enumerate(trace):
-            st = STATUS_BY_CODE[int(o["status"][i])]
-            done = st is Status.COMPLETED
-            outcomes.append(RequestOutcome(
+            st = by_code[int(o["status"][i])]
+            done = int(o["status"][i]) == N.COMPLETED
+            outcomes.append(fam.RequestOutcome(
                 id=req.id, status=st, ttft_slo=req.ttft_slo, tpot_slo=req.tpot_slo,
                 category=req.category,
                 first_token_time=float(o["first_token_time"][i]) if done else None,
@@ -192,16 +204,17 @@ def run_many(traces: list[list[Request]], configs: list[SimConfig], with_log: bo
                 ttft=float(o["ttft"][i]) if done else None,
                 tpot=float(o["tpot"][i]) if done else None,
                 slo_compliant=bool(o["compliant"][i])))
-        log = EventLog(sim_end_s=float(r["sim_end"]), engine_wall_s=wall, policy_wall_s=wall)
+        log = fam.EventLog(sim_end_s=float(r["sim_end"]), engine_wall_s=wall,
+                           policy_wall_s=wall)
         if with_log:
             _fill_log(log, eng.log(k), trace, cfg, dict(zip(arr.id.tolist(),
-                                                            arr.predicted.tolist())))
+                                                            arr.predicted.tolist())), fam)
         results.append((outcomes, log))
     return results
 
 
 def _fill_log(log: EventLog, lg: dict, trace: list[Request], cfg: SimConfig,
-              pred: dict[int, int]) -> None:
+              pred: dict[int, int], fam) -> None:
     by_id = {r.id: r for r in trace}
     tokens: dict[int, int] = {}
     running: list[int] = []
@@ -219,7 +232,7 @@ def _fill_log(log: EventLog, lg: dict, trace: list[Request], cfg: SimConfig,
             for q, rid in enumerate(adm):
                 v = lg["adm_rec"][ia + q]
                 r = by_id[rid]
-                recs.append(AdmissionRecord(
+                recs.append(fam.AdmissionRecord(
                     now=float(lg["now"][s]), candidate_id=rid, candidate_tpot_slo=r.tpot_slo,
                     candidate_len=r.prompt_len, predicted_len=int(pred[rid]),
                     running=tuple(snap),
@@ -229,7 +242,7 @@ def _fill_log(log: EventLog, lg: dict, trace: list[Request], cfg: SimConfig,
         ia, ir, ib = ia + na, ir + nr, ib + nb
         end = float(lg["end"][s])
         ms = float(lg["min_slo"][s])
-        log.steps.append(StepRecord(step=s, now_s=float(lg["now"][s]), end_s=end, admitted=adm,
+        log.steps.append(fam.StepRecord(step=s, now_s=float(lg["now"][s]), end_s=end, admitted=adm,
                                     rejected=rej, batch=bat, vbs=float(lg["vbs"][s]),
                                     min_slo_s=None if np.isnan(ms) else ms,
                                     prefill_s=float(lg["prefill_s"][s]),

@@ -67,6 +67,7 @@ def main() -> None:
     from slosim.sched_baselines import BaselineConfig
     from slosim.sched_scorpio import ScorpioConfig
     from slosim.seeds import derive_seed
+    from slosim.report import report_horizon, summarize
     from slosim.simengine import SimConfig, run
     from slosim.workload import LogNormalDist, UniformDist, WorkloadSpec, generate, rescale_arrivals
 
@@ -154,9 +155,37 @@ def main() -> None:
     add("single", [Request(id=0, arrival_time=0.0, prompt_len=100, true_output_len=3,
                            ttft_slo=0.5, tpot_slo=0.030, category=1)], itl=ex_itl, pre=ex_pre)
     add("empty", [], itl=ex_itl, pre=ex_pre)
+    # round 2: cost models the reference accepts but the fast kernel's monotone
+    # shortcuts do not cover -- negative ITL coefficients (fit_itl's lstsq may
+    # return them, costmodel.py:205; only epsilon is validated, :45-47) and a
+    # negative prefill slope (legal while alpha_p*theta + beta_p >= 0, :59-65;
+    # prompts past 500 tokens then get a negative prefill_time)
+    add("neg_gamma", ov[:900], itl=ItlParams(1e-6, 1e-3, -2e-6, 5e-3, 1.1))
+    add("neg_alpha", ov[:900], itl=ItlParams(-2e-8, 1e-3, 1e-5, 5e-3, 1.1))
+    add("neg_alpha_p", ov[:900], pre=PrefillParams(0.004, 128.0, -2e-6, 1e-3))
+    add("neg_alpha_p_early_reject", mid[:300], policy="early_reject", cap=8,
+        pre=PrefillParams(0.004, 128.0, -2e-6, 1e-3))
+    # dyadic everything: arrivals on a 1/64 s grid, power-of-two SLOs and cost
+    # coefficients, so walk and admission tests land exactly on their thresholds
+    dy_itl = ItlParams(2.0**-20, 2.0**-10, 2.0**-17, 2.0**-8, 1.0)
+    dy_pre = PrefillParams(2.0**-8, 128.0, 2.0**-16, 2.0**-9)
+    dy = []
+    rng = np.random.default_rng(23)
+    t = 0.0
+    for i in range(500):
+        t += float(rng.integers(0, 5)) / 64.0
+        dy.append(Request(id=i, arrival_time=t, prompt_len=int(rng.integers(1, 5)) * 64,
+                          true_output_len=int(rng.integers(1, 40)),
+                          ttft_slo=[0.25, 0.5, 1.0][i % 3], tpot_slo=[2.0**-5, 2.0**-4][i % 2],
+                          category=i % 3))
+    add("dyadic_ties", dy, itl=dy_itl, pre=dy_pre)
+    add("dyadic_ties_r_only", dy, itl=dy_itl, pre=dy_pre,
+        scorpio=ScorpioConfig(admission_min="r_only"))
 
     blobs = {}
     meta = []
+    reports = {}
+    jsonl = {}
     for ci, c in enumerate(cases):
         tr = c["trace"]
         cfg = SimConfig(policy=c["policy"], itl_params=c["itl"], prefill_params=c["pre"],
@@ -218,10 +247,22 @@ def main() -> None:
             n_steps=len(log.steps), n_idle_skips=len(log.idle_skips), sim_end=log.sim_end_s,
             digest=str(log_digest(log)), compliant=int(compliant), goodput=compliant / horizon,
             adherence=(compliant / len(outcomes)) if outcomes else 0.0, keep_log=c["keep_log"]))
+        # the reference's own RunReport and decision-log bytes (report.py:71-134,
+        # simengine.py:106-137) for the device report / log parity tests
+        reports[c["name"]] = summarize(outcomes, report_horizon(cfg.horizon, log)).to_dict()
+        if c["keep_log"] and len(tr) <= 1000:
+            jp = os.path.join(HERE, "_tmp.jsonl")
+            log.to_jsonl(jp)
+            with open(jp, "rb") as f:
+                jsonl[c["name"]] = np.frombuffer(f.read(), np.uint8)
+            os.remove(jp)
         print(f"{c['name']:>24}: n={len(tr)} steps={len(log.steps)} compliant={compliant}")
     np.savez_compressed(os.path.join(HERE, "sims.npz"), **blobs)
     with open(os.path.join(HERE, "sims.json"), "w") as f:
         json.dump(meta, f, indent=1)
+    with open(os.path.join(HERE, "reports.json"), "w") as f:
+        json.dump(reports, f)
+    np.savez_compressed(os.path.join(HERE, "decisions_jsonl.npz"), **jsonl)
 
     # ---- predictor KATs: numpy default_rng([seed, id]) stream (predictor.py:115-126)
     kat = {"seed": [], "id": [], "true_out": [], "num_buckets": [], "max_len": [],

@@ -135,3 +135,76 @@ def test_report_with_no_completions():
             assert len(series[k]) == 0 and rep[k].cumulative == []
         assert counts[k, :, 0].sum() == len(traces[cells[k].trace])
     assert (res["completed"] == 0).any()
+
+
+def test_report_and_jsonl_match_reference_bytes(golden):
+    """Every golden case through the device engine: summarize_batch().to_dict()
+    equals the reference's summarize(...).to_dict() (make_golden.py), key order
+    included (status_counts in first-occurrence order, report.py:104-106), and
+    run()'s EventLog.to_jsonl bytes equal the reference's (simengine.py:106-137)."""
+    import json
+    import os
+    import tempfile
+
+    from paper_2505_23022_b200.batch import BatchEngine, Cell, CellConfig, TraceArrays
+    from paper_2505_23022_b200.core import Request
+    from paper_2505_23022_b200.predictor import Bucketing, LengthPredictor
+    from paper_2505_23022_b200.report import summarize_batch
+    from paper_2505_23022_b200.sched_baselines import BaselineConfig
+    from paper_2505_23022_b200.sched_scorpio import ScorpioConfig
+    from paper_2505_23022_b200.costmodel import ItlParams, PrefillParams
+    from paper_2505_23022_b200.simengine import SimConfig, run_many
+    from tests._golden import HERE
+
+    want = json.load(open(os.path.join(HERE, "reports.json")))
+    jsonl = np.load(os.path.join(HERE, "decisions_jsonl.npz"))
+    traces, cells = [], []
+    for k, c in enumerate(golden):
+        t = c["trace"]
+        traces.append(TraceArrays(t["arrival"], t["ttft_slo"], t["tpot_slo"], t["prompt_len"],
+                                  t["true_out"], t["predicted"], t["id"], t["category"]))
+        cells.append(Cell(k, CellConfig(policy=c["policy"], itl=tuple(c["itl"]),
+                                        prefill=tuple(c["prefill"]), ttft_guard=c["ttft_guard"],
+                                        tpot_guard=c["tpot_guard"],
+                                        admission_min=c["admission_min"],
+                                        max_batch_size=c["max_batch_size"],
+                                        prefill_priority=c["prefill_priority"],
+                                        horizon=c["horizon"])))
+    eng = BatchEngine(traces, cells, outcomes=True)
+    eng.launch()
+    reps = summarize_batch(eng, traces)
+    for c, r in zip(golden, reps):
+        got = r.to_dict()
+        assert json.dumps(got) == json.dumps(want[c["name"]]), c["name"]
+    # decision-log bytes through the drop-in run() (device log -> EventLog)
+    jcases = [c for c in golden if c["name"] in jsonl.files]
+    assert len(jcases) >= 10
+    trs, cfgs = [], []
+    for c in jcases:
+        t = c["trace"]
+        trs.append([Request(id=int(t["id"][i]), arrival_time=float(t["arrival"][i]),
+                            prompt_len=int(t["prompt_len"][i]),
+                            true_output_len=int(t["true_out"][i]),
+                            ttft_slo=float(t["ttft_slo"][i]), tpot_slo=float(t["tpot_slo"][i]),
+                            category=int(t["category"][i])) for i in range(c["n"])])
+        pd = c["predictor"]
+        pred = LengthPredictor(mode=pd["mode"],
+                               bucketing=Bucketing.equal_width(pd["num_buckets"], pd["max_len"]),
+                               error_prob=pd["error_prob"], error_spread=pd["error_spread"],
+                               rng_seed=int(pd["rng_seed"]))
+        cfgs.append(SimConfig(policy=c["policy"], itl_params=ItlParams(*c["itl"]),
+                              prefill_params=PrefillParams(*c["prefill"]), predictor=pred,
+                              scorpio=ScorpioConfig(c["ttft_guard"], c["tpot_guard"],
+                                                    c["admission_min"]),
+                              baseline=BaselineConfig(max_batch_size=c["max_batch_size"],
+                                                      prefill_priority=c["prefill_priority"]),
+                              horizon=c["horizon"]))
+    for c, (outs, log) in zip(jcases, run_many(trs, cfgs)):
+        fd, p = tempfile.mkstemp(suffix=".jsonl")
+        os.close(fd)
+        try:
+            log.to_jsonl(p)
+            got = open(p, "rb").read()
+        finally:
+            os.remove(p)
+        assert got == jsonl[c["name"]].tobytes(), c["name"]
