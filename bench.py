@@ -1,7 +1,10 @@
 """Benchmark: Scorpio scheduler request-steps/s on B200 (config 3 / config 5 sweep).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU, NCCL)
+
+`--gpus N` (N > 1) without torchrun re-launches itself under
+`torch.distributed.run` with N ranks (one per GPU, NCCL) and fails loudly when
+fewer than N GPUs are visible; under torchrun WORLD_SIZE must equal N.
 
 One "step" = one pass of the hot path over one batch: every simulation cell of
 the rank's shard of the config-3 grid (64 request rates x 64 SLO scales of 10k
@@ -13,10 +16,18 @@ metric: request-steps/s, where one request-step = one waiting or running
 request at plan_step entry processed by one scheduler iteration of one sim
 (SURVEY 8(d)); the device counts them exactly per sim.
 
-`--impl reference` times the reference algorithm's CPU implementation (the C
-restatement under oracle/, the reference itself being pure Python that cannot
-travel to the GPU box) on all host threads over a bounded sample of the same
-cells and prints the same JSON line with "impl": "reference".
+`e2e` is the same metric through the public API from host arrays: each step
+packs the cell table (pack_cells), uploads traces + cells (BatchEngine), runs
+the sweep and reads the result rows back (plus the NCCL gather when N > 1),
+wall-clock timed with the device synchronised on both sides.
+
+`--impl reference` times the UNMODIFIED reference (`slosim`, pure Python,
+installed in baseline/_ref by tools/install_reference.sh) through its own
+`simengine.run` on every host core (multiprocessing.Pool), over a stratified
+sample of the same grid's cells with traces from the reference's own
+generator; request-steps per cell are counted by the C restatement (oracle/,
+parity-pinned) outside the timed region.  Without baseline/_ref it falls back
+to the C restatement itself (`kind: port`).
 """
 
 from __future__ import annotations
@@ -105,7 +116,7 @@ def make_grid(args, world: int):
 
 
 def sample_cells(grid, n_sample: int) -> list[tuple[int, int]]:
-    """Stratified (rate, scale) sample across the grid for the CPU baseline."""
+    """Stratified (rate, scale) sample across the grid for the CPU baselines."""
     nr, ns = len(grid.rates), len(grid.scales)
     side = max(1, int(round(np.sqrt(n_sample))))
     ri = np.unique(np.linspace(0, nr - 1, side).round().astype(int))
@@ -113,7 +124,44 @@ def sample_cells(grid, n_sample: int) -> list[tuple[int, int]]:
     return [(int(a), int(b)) for a in ri for b in si]
 
 
-def cpu_reference(grid, n_sample: int, budget_s: float, threads: int):
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_label(grid, world: int) -> dict:
+    """The workload the metric is quoted on -- identical in both arms."""
+    return {"workload": f"config{'5' if world > 1 else '3'}: {len(grid.rates)} rates x "
+                        f"{len(grid.scales)} SLO scales sweep, {grid.n_requests} requests/sim",
+            "sims": grid.n_cells, "n_requests": grid.n_requests,
+            "parallelism": f"sim-sharded x{world}", "l2": "flushed between steps"}
+
+
+def port_counts(grid, pairs, traces=None) -> dict:
+    """Request-steps of each sampled cell, from the C restatement (oracle/,
+    parity-pinned to the reference): the reference itself counts nothing."""
+    from oracle import oracle as orc
+
+    cfg = grid.config
+    params = orc.make_params(itl=cfg.itl, prefill=cfg.prefill)
+    traces = traces or {}
+    out = {}
+    for ri, si in pairs:
+        t = traces.get(ri) or grid.trace_for_rate(grid.rates[ri])
+        traces[ri] = t
+        sc = float(grid.scales[si])
+        r = orc.run_sim(t.arrival, t.ttft_slo * sc, t.tpot_slo * sc, t.prompt_len, t.true_out,
+                        t.id, t.predicted, params)
+        out[(ri, si)] = int(r["summary"]["request_steps"])
+    return out
+
+
+def cpu_port(grid, n_sample: int, budget_s: float, threads: int):
     """Time the C restatement (oracle/) on all host threads over a sample of the
     grid's cells (stratified rate x scale; every cell when n_sample >= cells),
     scheduled longest-first on a thread pool (ctypes drops the GIL per sim).
@@ -150,27 +198,132 @@ def cpu_reference(grid, n_sample: int, budget_s: float, threads: int):
                                    f"(rate x scale), {grid.n_requests} requests each"
 
 
+# ---- the unmodified reference (slosim, pure Python) in worker processes
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_REF_TRACES: dict = {}
+
+
+def _ref_init(ref_dir: str, rates: list, n_requests: int) -> None:
+    """Worker start-up (outside the timed region): import slosim from
+    baseline/_ref and draw the sampled rates' traces with the reference's own
+    generator (report.py:167-177 seeds)."""
+    sys.path.insert(0, ref_dir)
+    import logging
+
+    logging.disable(logging.WARNING)
+    from slosim.seeds import derive_seed
+    from slosim.workload import LogNormalDist, WorkloadSpec, generate
+
+    for q in rates:
+        spec = WorkloadSpec(qps=float(q), duration=1.1 * n_requests / float(q),
+                            seed=derive_seed(0, "trace", float(q)),
+                            prompt_len_dist=LogNormalDist(5.0, 0.7),
+                            output_len_dist=LogNormalDist(4.0, 0.7),
+                            category_weights=(1.0,) * 6)
+        _REF_TRACES[float(q)] = generate(spec)[:n_requests]
+
+
+def _ref_ready(_) -> int:
+    time.sleep(0.05)
+    return os.getpid()
+
+
+def _ref_cell(task) -> tuple[int, int]:
+    """One cell through slosim.simengine.run: the SLO scale multiplies both
+    thresholds of every request."""
+    q, sc, itl, pre = task
+    from slosim.core import Request
+    from slosim.costmodel import ItlParams, PrefillParams
+    from slosim.predictor import Bucketing, LengthPredictor
+    from slosim.sched_baselines import BaselineConfig
+    from slosim.simengine import SimConfig, run
+
+    tr = [Request(id=r.id, arrival_time=r.arrival_time, prompt_len=r.prompt_len,
+                  true_output_len=r.true_output_len, ttft_slo=r.ttft_slo * sc,
+                  tpot_slo=r.tpot_slo * sc, category=r.category) for r in _REF_TRACES[q]]
+    cfg = SimConfig(policy="scorpio", itl_params=ItlParams(*itl), prefill_params=PrefillParams(*pre),
+                    predictor=LengthPredictor(mode="oracle",
+                                              bucketing=Bucketing.equal_width(100, 4096)),
+                    baseline=BaselineConfig(max_batch_size=256))
+    outcomes, _ = run(tr, cfg)
+    return len(outcomes), sum(1 for o in outcomes if o.slo_compliant)
+
+
+class PythonReference:
+    """A process pool (one worker per host core) running the reference over a
+    stratified sample of the grid; each `step()` runs the whole sample, cells
+    handed out one at a time, lowest rate (longest step chain) first."""
+
+    def __init__(self, grid, cores: int, n_sample: int = 64):
+        import multiprocessing as mp
+
+        self.grid, self.cores = grid, cores
+        self.pairs = sorted(sample_cells(grid, n_sample), key=lambda p: (p[0], p[1]))
+        rates = sorted({float(grid.rates[ri]) for ri, _ in self.pairs})
+        self.counts = port_counts(grid, self.pairs)
+        self.pool = mp.get_context("spawn").Pool(cores, initializer=_ref_init,
+                                                 initargs=(REF_DIR, rates, grid.n_requests))
+        # every worker initialised (traces drawn) before any timing: a worker runs
+        # tasks only after its initializer, so seeing every pid proves it
+        pids: set = set()
+        for _ in range(200):
+            pids |= set(self.pool.map(_ref_ready, range(4 * cores), chunksize=1))
+            if len(pids) >= cores:
+                break
+
+    def step(self) -> tuple[int, float]:
+        cfg = self.grid.config
+        tasks = [(float(self.grid.rates[ri]), float(self.grid.scales[si]), tuple(cfg.itl),
+                  tuple(cfg.prefill)) for ri, si in self.pairs]
+        t0 = time.perf_counter()
+        self.pool.map(_ref_cell, tasks, chunksize=1)
+        dt = time.perf_counter() - t0
+        return sum(self.counts.values()), dt
+
+    def close(self) -> None:
+        self.pool.terminate()
+        self.pool.join()
+
+
 def run_reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    threads = len(os.sched_getaffinity(0))
-    grid = make_grid(args, 1)
+    cores = len(os.sched_getaffinity(0))
+    world = args.gpus
+    grid = make_grid(args, world)
+    have_ref = os.path.isdir(os.path.join(REF_DIR, "slosim"))
     steps_rs, steps_dt = [], []
-    desc = ""
-    for it in range(args.warmup + args.steps):
-        rs, dt, n, desc = cpu_reference(grid, args.cpu_sample, args.ref_budget, threads)
-        if it >= args.warmup:
-            steps_rs.append(rs)
-            steps_dt.append(dt)
+    if have_ref:
+        ref = PythonReference(grid, cores, args.ref_sample)
+        for it in range(args.warmup + args.steps):
+            rs, dt = ref.step()
+            if it >= args.warmup:
+                steps_rs.append(rs)
+                steps_dt.append(dt)
+        ref.close()
+        kind = "reference"
+        desc = (f"slosim.simengine.run (unmodified, baseline/_ref) on {cores} processes: each "
+                f"step runs a stratified {len(ref.pairs)}-cell sample of the {grid.n_cells}-cell "
+                f"grid (lowest rate first, one cell per task), {grid.n_requests} requests each; "
+                f"request-steps per cell counted by the parity-pinned C restatement outside "
+                f"the timed region")
+    else:  # no reference install: the C restatement (oracle/)
+        for it in range(args.warmup + args.steps):
+            rs, dt, n, desc = cpu_port(grid, args.cpu_sample, args.ref_budget, cores)
+            if it >= args.warmup:
+                steps_rs.append(rs)
+                steps_dt.append(dt)
+        kind = "port"
     value = sum(steps_rs) / sum(steps_dt)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(steps_dt) / len(steps_dt), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
-            "config": {"workload": "config3 sweep sample", "n_requests": grid.n_requests},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": desc},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64",
+            "data": "synthetic (reference workload generator, seeded)",
+            "config": config_label(grid, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": desc, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -408,16 +561,35 @@ def baselines_bench(grid, dev) -> dict:
     return out
 
 
+def sim_kernel_profile(n_requests: int, cells: int) -> dict | None:
+    """The committed ncu capture of the hot sweep kernel for this workload
+    (profiles/sim_kernel_ncu.json: DRAM bytes, warp instructions, duration, SM
+    clock of one `ncu --set full --clock-control none` launch)."""
+    prof = os.path.join(ROOT, "profiles", "sim_kernel_ncu.json")
+    if not os.path.exists(prof):
+        return None
+    p = json.load(open(prof))
+    if p.get("n_requests") != n_requests or p.get("cells") != cells:
+        return None
+    return p
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
 
     from paper_2505_23022_b200 import _native as N
+    from paper_2505_23022_b200.batch import BatchEngine
     from paper_2505_23022_b200.sweep import build_local, gather_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        sys.exit(f"bench.py: {world} ranks need {world} GPUs, "
+                 f"{torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -468,29 +640,31 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
         ktimes.append(e0.elapsed_time(e1) / 1e3)
 
-    # e2e: public API with host buffers; H2D of inputs + launch + D2H of result rows
-    pinned = {k: v.cpu().pin_memory() for k, v in eng._tr.items()}
-    sims_pinned = eng._sims.cpu().pin_memory()
-    res_pinned = torch.empty(eng._res.numel(), dtype=torch.uint8).pin_memory()
-    h2d = sum(v.numel() * v.element_size() for v in pinned.values()) + sims_pinned.numel()
-    d2h = res_pinned.numel()
+    # e2e: the public API from host arrays, every step: pack the cell table,
+    # upload traces + cells (BatchEngine), sweep, read the result rows back
+    # (+ gather when N > 1); wall clock with the device synchronised both sides
+    cells = build_cells(grid, owned, traces)
+    h2d = sum(getattr(t, k).nbytes for t in traces for k in
+              ("arrival", "ttft_slo", "tpot_slo", "prompt_len", "true_out", "predicted", "id"))
+    h2d += 8 * (len(traces) + 1) + len(cells) * (N.SIM_DTYPE.itemsize + 4)  # + begin, order
+    d2h = len(cells) * N.RESULT_DTYPE.itemsize
     etimes = []
-    for _ in range(args.steps):
+    for it in range(args.warmup + args.steps):
         l2.zero_()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for k, v in pinned.items():
-            eng._tr[k].copy_(v, non_blocking=True)
-        eng._sims.copy_(sims_pinned, non_blocking=True)
-        one_step()
-        res_pinned.copy_(eng._res, non_blocking=True)
-        e1.record(stream)
+        t0 = time.perf_counter()
+        e = BatchEngine(traces, cells, device=dev)
+        e.launch(stream)
+        rows = e.results()  # D2H of the result rows (synchronises)
+        if world > 1:
+            gather_rows(e.results_device(), owned, grid.n_cells)
         torch.cuda.synchronize()
-        etimes.append(e0.elapsed_time(e1) / 1e3)
+        if it >= args.warmup:
+            etimes.append(time.perf_counter() - t0)
+        assert int(rows["request_steps"].sum()) == local_rs
+        del e
 
     t_step = float(np.mean(times))
     t_kernel = float(np.mean(ktimes))
@@ -508,38 +682,52 @@ def run_ours(args) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        rs, dt, ncell, desc = cpu_reference(grid, args.cpu_sample, args.cpu_budget, threads)
-        cpu = {"value": rs / dt, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+        rs, dt, ncell, desc = cpu_port(grid, args.cpu_sample, args.cpu_budget, threads)
+        cpu = {"value": rs / dt, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc,
+               "cpu_model": cpu_model()}
+        if os.path.isdir(os.path.join(REF_DIR, "slosim")):
+            ref = PythonReference(grid, threads, args.ref_sample)
+            rrs, rdt = ref.step()
+            ref.close()
+            cpu["reference_python"] = {
+                "value": rrs / rdt, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"a stratified {len(ref.pairs)}-cell sample through "
+                          f"slosim.simengine.run (unmodified, baseline/_ref), one cell per task "
+                          f"on {threads} processes"}
 
     if rank == 0:
         peak, src = peaks()
         achieved = local_rs * BYTES_PER_REQUEST_STEP / t_kernel / 1e9
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "sim_kernel_traffic.json")
-        if os.path.exists(prof):
-            p = json.load(open(prof))
-            if p.get("n_requests") == args.n_requests and p.get("cells") == eng.n_sims:
-                traffic = p.get("dram_bytes")
+        prof = sim_kernel_profile(args.n_requests, eng.n_sims)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": src,
+                "bytes_per_unit": BYTES_PER_REQUEST_STEP,
+                "kernel": "sl_sim_fast_kernel<hot> (+ WRec pre-pass and 2 handoff launches)",
+                "kernel_ms": 1e3 * t_kernel}
+        if prof is not None:
+            dur = prof["gpu_time_ns"] * 1e-9
+            roof["traffic"] = prof["dram_bytes"]
+            # measured-DRAM fraction and issue-slot fraction of the same launch
+            # (ncu, profiles/sim_kernel_ncu.json): the kernel is issue/latency bound
+            roof["dram_frac"] = prof["dram_bytes"] / dur / 1e9 / peak
+            roof["issue_frac"] = prof["inst_executed"] / (
+                prof["sms"] * 4 * prof["sm_clock_hz"] * dur)
+            roof["ncu"] = {k: prof[k] for k in ("inst_executed", "gpu_time_ns", "dram_bytes",
+                                                "sm_clock_hz", "source")}
         line = {
             "metric": METRIC, "value": total_rs / t_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64+int64", "data": "synthetic (reference workload generator, seeded)",
-            "config": {"workload": f"config{'5' if world > 1 else '3'}: "
-                                   f"{len(grid.rates)} rates x {len(grid.scales)} SLO scales "
-                                   f"sweep, {grid.n_requests} requests/sim",
-                       "sims": grid.n_cells, "sims_per_gpu": eng.n_sims,
-                       "n_requests": grid.n_requests, "request_steps": total_rs,
-                       "parallelism": f"sim-sharded x{world}", "l2": "flushed between steps",
-                       "setup_s": round(setup_s, 2)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": src,
-                         "bytes_per_unit": BYTES_PER_REQUEST_STEP,
-                         "kernel": "sl_sim_fast_kernel<hot> (+2 empty handoff launches)",
-                         "kernel_ms": 1e3 * t_kernel},
+            "config": config_label(grid, world),
+            "workload_detail": {"sims_per_gpu": eng.n_sims, "request_steps": total_rs,
+                                "setup_s": round(setup_s, 2)},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": total_rs / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e,
+                    "timed": "pack_cells + BatchEngine upload from host arrays + sweep + "
+                             "result-row read-back (+ gather), wall clock"},
             "gpu_launches": args.steps * N.lib().sl_run_batch_launches(),
             "clocks": clk.summary(),
         }
@@ -557,6 +745,35 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def build_cells(grid, owned, traces):
+    """The Cell list build_local made for this rank (same order)."""
+    from paper_2505_23022_b200.batch import Cell
+
+    need = sorted({int(c) // len(grid.scales) for c in owned})
+    tix = {ri: k for k, ri in enumerate(need)}
+    return [Cell(tix[int(c) // len(grid.scales)], grid.config,
+                 slo_scale=float(grid.scales[int(c) % len(grid.scales)])) for c in owned]
+
+
+def relaunch_distributed(n: int) -> None:
+    """`bench.py --gpus N` outside torchrun: N ranks under torch.distributed.run
+    (one per GPU, rendezvous on 127.0.0.1), or a loud failure without N GPUs."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        sys.exit(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -568,10 +785,12 @@ def main() -> None:
     ap.add_argument("--n-requests", type=int, default=10_000)
     ap.add_argument("--cpu-sample", type=int, default=4096,
                     help="cells timed for cpu_baseline (>= grid size: the whole grid)")
-    ap.add_argument("--cpu-budget", type=float, default=25.0,
+    ap.add_argument("--cpu-budget", type=float, default=15.0,
                     help="wall seconds after which the cpu_baseline stops submitting cells")
     ap.add_argument("--ref-budget", type=float, default=12.0,
-                    help="wall seconds per --impl reference step (same cell order)")
+                    help="wall seconds per --impl reference step (C-port fallback only)")
+    ap.add_argument("--ref-sample", type=int, default=32,
+                    help="stratified cells the Python reference cycles through")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-plan", action="store_true", help="skip the config-2 plan microbench")
     ap.add_argument("--no-config4", action="store_true",
@@ -581,8 +800,12 @@ def main() -> None:
     ap.add_argument("--no-report", action="store_true",
                     help="skip the device RunReport timing (config-3 sweep with outcomes)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
     else:
         run_ours(args)
 

@@ -255,7 +255,7 @@ class BatchEngine:
         if order is None:
             order = default_order(traces, sims)
         self._sims = up(sims.view(np.uint8))
-        self.total_slots = int(sum(lens[s["trace"]] for s in sims)) if len(sims) else 0
+        self.total_slots = int(lens[sims["trace"].astype(np.int64)].sum()) if len(sims) else 0
         wsb = N.lib().sl_workspace_bytes(self.total_slots, self.n_sims)
         self._ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         self._res = torch.zeros(self.n_sims * N.RESULT_DTYPE.itemsize, dtype=torch.uint8,
@@ -427,13 +427,14 @@ def default_order(traces: list[TraceArrays], sims: np.ndarray) -> np.ndarray:
     longest step chains, so they start first."""
     if len(sims) == 0:
         return np.zeros(0, np.int32)
-    rate = np.empty(len(sims))
-    for k, s in enumerate(sims):
-        t = traces[s["trace"]]
-        span = float(t.arrival[-1]) / float(s["rate_factor"]) if len(t) else 0.0
-        rate[k] = len(t) / span if span > 0 else np.inf
+    n_tr = np.array([len(t) for t in traces], np.float64)
+    last = np.array([float(t.arrival[-1]) if len(t) else 0.0 for t in traces])
+    ti = sims["trace"].astype(np.int64)
+    span = last[ti] / sims["rate_factor"]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rate = np.where(span > 0, n_tr[ti] / np.where(span > 0, span, 1.0), np.inf)
     # low rate first; ties by larger trace first
-    key = np.lexsort((-np.array([len(traces[s["trace"]]) for s in sims]), rate))
+    key = np.lexsort((-n_tr[ti], rate))
     return key.astype(np.int32)
 
 
