@@ -339,8 +339,8 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
     fused single-launch plan step (segments <= 32 waiting) as a whole; each launch
     alone on the stream (enqueued behind a GPU sleep so no host launch overhead
     is timed), L2 flushed before each.  Compulsory bytes (each input read once,
-    each output written once): sort 24 B read (arrival, ttft, id) + 4 B written
-    (perm) per waiting item; scan 44 B read (perm, arrival, prefill, ttft, tpot,
+    each output written once): sort 16 B read (arrival, ttft: the deadline key;
+    the id is read only on deadline ties) + 4 B written (perm) per waiting item; scan 44 B read (perm, arrival, prefill, ttft, tpot,
     prompt, predicted) + 8 B written (status, position) per waiting item and 12 B
     read (tpot, current length) per running item (admission records of admitted
     items not counted); select 17 B read (tpot, credit, exclude) + 13 B written
@@ -380,7 +380,7 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
                 torch.cuda.synchronize()
                 if it >= 2:
                     times[k].append(e0.elapsed_time(e1) / 1e3)
-        bytes_ = {"sort": 28 * Wt, "scan": 52 * Wt + 12 * Rt, "select": 30 * Rt,
+        bytes_ = {"sort": 20 * Wt, "scan": 52 * Wt + 12 * Rt, "select": 30 * Rt,
                   "fused": 60 * Wt + 34 * Rt}
         rows = {}
         for k in phases:

@@ -391,6 +391,15 @@ class BatchEngine:
             raise RuntimeError("engine built without outcomes")
         return {k: v[: self.total_slots].cpu().numpy() for k, v in self._out.items()}
 
+    def cell_outcomes(self, k: int) -> dict[str, np.ndarray]:
+        """Outcome arrays of cell k, copied from the device slice alone."""
+        if not self.has_outcomes:
+            raise RuntimeError("engine built without outcomes")
+        s = self.sims_host[k]
+        b = int(s["out_offset"])
+        n = int(self.trace_begin[s["trace"] + 1] - self.trace_begin[s["trace"]])
+        return {f: v[b:b + n].cpu().numpy() for f, v in self._out.items()}
+
     def sim_outcomes(self, k: int, all_out: dict | None = None) -> dict[str, np.ndarray]:
         """Outcome arrays of cell k (slices of outcomes())."""
         all_out = all_out if all_out is not None else self.outcomes()

@@ -61,7 +61,9 @@ def config2_arrays(n_segments: int, w: int, r: int, seed: int, now: float = 10.0
 def config2_plan_arrays_fast(n_segments: int, w: int, r: int, seed: int, now: float = 10.0,
                             prefill=ACC_PREFILL) -> dict[str, np.ndarray]:
     """Vectorised sl_plan_state SoA with config2_arrays' distributions (a different
-    random stream) for large benchmark batches; not used for parity fixtures."""
+    random stream) for large benchmark batches; bench.py times these, and 256
+    segments of the 262,144-segment batch are pinned to the reference's
+    plan_step (tests/golden/make_plan_golden.py, states_from_plan_arrays)."""
     rng = np.random.default_rng(seed)
     S, W, R = n_segments, n_segments * w, n_segments * r
     ttft = np.array([t[0] for t in TIERS])
@@ -123,6 +125,38 @@ def states_from_arrays(a: dict, types) -> list:
             e = types.RunningEntry(request=req, predicted_len=int(a["r_out"][j]), prefill_s=0.0)
             e.tokens_generated = int(a["r_tokens"][j])
             e.credit = Fraction(int(a["r_credit_num"][j])) * Fraction(2) ** E / \
+                Fraction(float(a["r_tpot"][j]))
+            st.running.append(e)
+        out.append(st)
+    return out
+
+
+def states_from_plan_arrays(a: dict, types, segments) -> list:
+    """SchedulerState objects for selected segments of an sl_plan_state SoA
+    (e.g. config2_plan_arrays_fast): a running entry's current length is split
+    as prompt = cur_len - 1 plus one generated token (plan_step reads only the
+    sum), its credit restored exactly from the fixed-point numerator."""
+    from fractions import Fraction
+
+    E = int(a["credit_exp"][0])
+    out = []
+    for s in segments:
+        st = types.SchedulerState(now=float(a["now"][s]))
+        for i in range(int(a["w_begin"][s]), int(a["w_begin"][s + 1])):
+            req = types.Request(id=int(a["w_id"][i]), arrival_time=float(a["w_arrival"][i]),
+                                prompt_len=int(a["w_prompt"][i]),
+                                true_output_len=int(a["w_pred"][i]),
+                                ttft_slo=float(a["w_ttft"][i]), tpot_slo=float(a["w_tpot"][i]))
+            st.waiting.append(types.WaitingItem(request=req, predicted_len=int(a["w_pred"][i]),
+                                                prefill_s=float(a["w_prefill"][i])))
+        for j in range(int(a["r_begin"][s]), int(a["r_begin"][s + 1])):
+            cur = int(a["r_cur_len"][j])
+            req = types.Request(id=int(a["r_id"][j]), arrival_time=0.0, prompt_len=cur - 1,
+                                true_output_len=cur + 1000, ttft_slo=1.0,
+                                tpot_slo=float(a["r_tpot"][j]))
+            e = types.RunningEntry(request=req, predicted_len=400, prefill_s=0.0)
+            e.tokens_generated = 1
+            e.credit = Fraction(int(a["r_credit"][j])) * Fraction(2) ** E / \
                 Fraction(float(a["r_tpot"][j]))
             st.running.append(e)
         out.append(st)

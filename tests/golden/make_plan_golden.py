@@ -26,7 +26,13 @@ CASES = [  # (name, segments, W, R, seed, flags)
     ("neither", 16, 32, 32, 7, "neither"),
     ("tile_merge_5000", 1, 5000, 300, 8, "both"),
     ("stress_32768", 1, 32768, 32768, 9, "both"),
+    # the shapes bench.py times (config 2): the primary batch exactly ...
+    ("bench_primary_1024", 1024, 32, 32, 11, "both"),
 ]
+# ... and 256 segments spread over the bench's 262,144-segment scaled batch
+# (config2_plan_arrays_fast, seed 11): the test runs the whole batch through the
+# same kernels the bench times and compares the sampled segments
+SAMPLED = [("bench_scaled_262144", 262144, 32, 32, 11, "both", 256)]
 
 
 def main() -> None:
@@ -38,7 +44,8 @@ def main() -> None:
     from slosim.predictor import Bucketing, LengthPredictor
     from slosim.sched_scorpio import ScorpioConfig, plan_step
 
-    from paper_2505_23022_b200.snapshot import config2_arrays, states_from_arrays
+    from paper_2505_23022_b200.snapshot import (config2_arrays, config2_plan_arrays_fast,
+                                                 states_from_arrays, states_from_plan_arrays)
 
     T = types.SimpleNamespace(Request=core.Request, WaitingItem=schedtypes.WaitingItem,
                               RunningEntry=schedtypes.RunningEntry,
@@ -50,9 +57,16 @@ def main() -> None:
             "ttft_only": ScorpioConfig(tpot_guard=False), "tpot_only": ScorpioConfig(ttft_guard=False),
             "neither": ScorpioConfig(False, False)}
     blobs, meta = {}, []
-    for name, S, W, R, seed, fl in CASES:
-        a = config2_arrays(S, W, R, seed)
-        states = states_from_arrays(a, T)
+    jobs = [(name, S, W, R, seed, fl, None) for name, S, W, R, seed, fl in CASES] + SAMPLED
+    for name, S, W, R, seed, fl, n_sample in jobs:
+        if n_sample is None:
+            a = config2_arrays(S, W, R, seed)
+            states = states_from_arrays(a, T)
+            segs = None
+        else:
+            a = config2_plan_arrays_fast(S, W, R, seed)
+            segs = [int(x) for x in np.linspace(0, S - 1, n_sample).round()]
+            states = states_from_plan_arrays(a, T, segs)
         adm, rej, bat, wait, vbs, mins, cred = [], [], [], [], [], [], []
         for st in states:
             p = plan_step(st, pred, itl, pre, cfgs[fl])
@@ -75,7 +89,7 @@ def main() -> None:
         blobs[k + "vbs"] = np.array(vbs)
         blobs[k + "min_slo"] = np.array(mins)
         blobs[k + "credit"] = np.array(cred, np.uint64)
-        meta.append(dict(name=name, segments=S, w=W, r=R, seed=seed, flags=fl))
+        meta.append(dict(name=name, segments=S, w=W, r=R, seed=seed, flags=fl, sample=segs))
         print(name, "admitted", sum(map(len, adm)), "rejected", sum(map(len, rej)),
               "batch", sum(map(len, bat)))
     np.savez_compressed(os.path.join(HERE, "plan.npz"), **blobs)

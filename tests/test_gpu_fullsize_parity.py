@@ -6,9 +6,23 @@
   compliant / sim_end, adherence == compliant / total, no engine error, request
   steps >= steps);
 * 48 stratified cells (every rate row, scales spread over the axis, the 2 req/s
-  critical-path cells included): every result-row field and the work-step
-  digest bit-exact against the C oracle on the same traces.
+  critical-path cells included): every result-row field, the work-step digest
+  and every request's outcome (status, completion step, first-token and
+  completion times, TTFT, TPOT, compliance) bit-exact against the C oracle on
+  the same traces.
 """
+
+OUTCOME_FIELDS = ("status", "compliant", "completion_step", "first_token_time",
+                  "completion_time", "ttft", "tpot")
+
+
+def assert_outcomes_equal(got, ref, where):
+    for f in OUTCOME_FIELDS:
+        a, b = np.asarray(got[f]), np.asarray(ref[f])
+        if a.dtype.kind == "f":
+            assert same_float(a, b), (where, f)
+        else:
+            assert np.array_equal(a, b), (where, f, int((a != b).sum()))
 
 import numpy as np
 import pytest
@@ -29,13 +43,13 @@ def config3():
     from paper_2505_23022_b200.sweep import SweepGrid, build_local
 
     grid = SweepGrid()  # the bench's config-3 grid
-    eng, owned, traces = build_local(grid, device=torch.device("cuda", 0))
+    eng, owned, traces = build_local(grid, outcomes=True, device=torch.device("cuda", 0))
     eng.launch()
-    return grid, eng.results(), traces
+    return grid, eng.results(), traces, eng
 
 
 def test_config3_invariants_every_cell(config3):
-    grid, res, _ = config3
+    grid, res, _, _ = config3
     assert len(res) == 4096
     assert ((res["status"] & 3) == 0).all()
     n = res["total"]
@@ -55,7 +69,7 @@ def test_config3_invariants_every_cell(config3):
 def test_config3_sampled_cells_match_oracle(config3):
     from oracle import oracle as orc
 
-    grid, res, traces = config3
+    grid, res, traces, eng = config3
     ns = len(grid.scales)
     scale_pick = [0, 9, 21, 32, 45, 63]
     rate_pick = list(range(0, 64, 8)) + [1, 63]
@@ -76,6 +90,7 @@ def test_config3_sampled_cells_match_oracle(config3):
         for f in ("sim_end", "goodput", "adherence"):
             assert same_float([r[f]], [sm[f]]), (ri, si, f)
         assert int(r["digest"]) == sm["digest"], (ri, si)
+        assert_outcomes_equal(eng.cell_outcomes(ri * ns + si), ref, (ri, si))
 
 
 def test_config4_sampled_cells_match_oracle():
@@ -107,7 +122,7 @@ def test_config4_sampled_cells_match_oracle():
         t.predicted = p[k: k + len(t)].copy()
         k += len(t)
     cells = [Cell(ri, grid.config, slo_scale=float(sc)) for ri in range(128) for sc in grid.scales]
-    eng = BatchEngine(traces, cells, device=dev)
+    eng = BatchEngine(traces, cells, outcomes=True, device=dev)
     eng.launch()
     res = eng.results()
     assert ((res["status"] & 3) == 0).all()
@@ -126,3 +141,4 @@ def test_config4_sampled_cells_match_oracle():
         for f in FIELDS:
             assert r[f] == sm[f], (ri, si, f, r[f], sm[f])
         assert same_float([r["goodput"]], [sm["goodput"]]) and int(r["digest"]) == sm["digest"]
+        assert_outcomes_equal(eng.cell_outcomes(ri * 128 + si), ref, (ri, si))
