@@ -645,29 +645,37 @@ __global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_confi
 }
 
 // Few, large segments (the config-2 stress shape): one 1024-thread CTA per
-// segment instead of one warp, tiles of 1024 entries, batch positions by a
-// CTA-wide ballot scan -- the same per-entry arithmetic as seg_credit_select.
+// segment instead of one warp.  Entries go in super-tiles of 32 x 1024: pass 1
+// earns / debits every entry (coalesced) and keeps its batch bit in a register,
+// one count per (tile, warp) in shared memory; one CTA-wide scan of the 1,024
+// counts; pass 2 writes the batch positions.  Same per-entry arithmetic as
+// seg_credit_select.
 constexpr int kSelCta = 1024;
 __global__ void __launch_bounds__(kSelCta) credit_select_cta_kernel(const sl_plan_state st,
                                                                     const sl_plan_config cfg,
                                                                     sl_plan_out out,
                                                                     int use_seg_min) {
-  __shared__ unsigned wcnt[kSelCta / 32];
+  __shared__ int cnt[kSelCta];
+  __shared__ int wtot[32];
   __shared__ unsigned long long smin;
+  __shared__ int sbase;
   const int seg = blockIdx.x;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const bool credit = cfg.flags & SL_FLAG_TPOT_GUARD;
   const int64_t rb = st.r_begin[seg];
   const int R = (int)(st.r_begin[seg + 1] - rb);
   const int E = st.credit_exp[seg];
-  if (threadIdx.x == 0) smin = ~0ull;
+  if (tid == 0) {
+    smin = ~0ull;
+    sbase = 0;
+  }
   __syncthreads();
   if (credit) {
     if (use_seg_min) {
-      if (threadIdx.x == 0) smin = out.seg_min_fixed[seg];
+      if (tid == 0) smin = out.seg_min_fixed[seg];
     } else {
       uint64_t m = ~0ull;
-      for (int j = threadIdx.x; j < R; j += kSelCta) {
+      for (int j = tid; j < R; j += kSelCta) {
         const uint64_t S = slo_fixed<false>(st.r_tpot[rb + j], E);
         m = S < m ? S : m;
       }
@@ -677,42 +685,70 @@ __global__ void __launch_bounds__(kSelCta) credit_select_cta_kernel(const sl_pla
   }
   __syncthreads();
   const uint64_t MIN = smin;
-  int nb = 0;
-  for (int c0 = 0; c0 < R; c0 += kSelCta) {
-    const int j = c0 + threadIdx.x;
-    bool b = false;
-    if (j < R) {
-      const int64_t r = rb + j;
-      const bool ex = st.r_exclude && st.r_exclude[r];
-      uint64_t N = st.r_credit[r];
-      if (!ex) {
-        if (credit) {
-          const uint64_t S = slo_fixed<false>(st.r_tpot[r], E);
-          N += MIN;
-          b = N >= S;
-          if (b) N -= S;
-        } else {
-          b = true;
+  constexpr int kSuper = 32 * kSelCta;
+  for (int s0 = 0; s0 < R; s0 += kSuper) {
+    unsigned bits = 0;
+#pragma unroll 4
+    for (int it = 0; it < 32; ++it) {
+      const int j = s0 + it * kSelCta + tid;
+      bool b = false;
+      if (j < R) {
+        const int64_t r = rb + j;
+        const bool ex = st.r_exclude && st.r_exclude[r];
+        uint64_t N = st.r_credit[r];
+        if (!ex) {
+          if (credit) {
+            const uint64_t S = slo_fixed<false>(st.r_tpot[r], E);
+            N += MIN;
+            b = N >= S;
+            if (b) N -= S;
+          } else {
+            b = true;
+          }
         }
+        out.r_credit_out[r] = N;
+        out.r_batch[r] = b;
       }
-      out.r_credit_out[r] = N;
+      bits |= (unsigned)b << it;
+      const unsigned bm = __ballot_sync(SL_FULL, b);
+      if (lane == 0) cnt[it * 32 + w] = __popc(bm);
     }
-    const unsigned bm = __ballot_sync(SL_FULL, b);
-    if (lane == 0) wcnt[w] = __popc(bm);
     __syncthreads();
-    int before = 0, tot = 0;
-    for (int q = 0; q < kSelCta / 32; ++q) {
-      before += q < w ? (int)wcnt[q] : 0;
-      tot += (int)wcnt[q];
+    // exclusive scan of cnt[0..1023] (tile-major, warp-minor = entry order)
+    const int v = cnt[tid];
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(SL_FULL, x, o);
+      if (lane >= o) x += y;
     }
-    if (j < R) {
-      out.r_batch[rb + j] = b;
-      out.r_pos[rb + j] = b ? nb + before + __popc(bm & lanemask_lt()) : -1;
+    if (lane == 31) wtot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = wtot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(SL_FULL, t, o);
+        if (lane >= o) t += y;
+      }
+      wtot[lane] = t;  // inclusive
     }
-    nb += tot;
+    __syncthreads();
+    const int base = sbase;
+    cnt[tid] = base + (w ? wtot[w - 1] : 0) + x - v;
+    __syncthreads();
+#pragma unroll 4
+    for (int it = 0; it < 32; ++it) {
+      const int j = s0 + it * kSelCta + tid;
+      const bool b = (bits >> it) & 1u;
+      const unsigned bm = __ballot_sync(SL_FULL, b);
+      if (j < R) out.r_pos[rb + j] = b ? cnt[it * 32 + w] + __popc(bm & lanemask_lt()) : -1;
+    }
+    __syncthreads();
+    if (tid == 0) sbase = base + wtot[31];
     __syncthreads();
   }
-  if (threadIdx.x == 0) out.seg_counts[4 * seg + 3] = nb;
+  if (tid == 0) out.seg_counts[4 * seg + 3] = sbase;
 }
 
 // Segment count below which credit select runs one CTA per segment.
@@ -767,7 +803,16 @@ int plan_group_min() {
   return 8192;
 }
 
+// Segment count up to which guard + admission runs one CTA per segment
+// (guard_admit_cta_kernel, plan_large.cuh); SL_PLAN_CTA_MAX overrides it.
+int plan_cta_max() {
+  if (const char* e = getenv("SL_PLAN_CTA_MAX")) return atoi(e);
+  return kSelCtaMaxSegments;
+}
+
 }  // namespace
+
+#include "plan_large.cuh"
 
 extern "C" {
 
@@ -810,6 +855,15 @@ int sl_guard_admit_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_
     return SL_ERR_ARG;
   if ((cfg->flags & SL_FLAG_TTFT_GUARD) && !out->perm) return SL_ERR_ARG;
   if (st->n_segments == 0) return SL_OK;
+  if (st->n_segments <= plan_cta_max()) {
+    const int smem = (int)sizeof(LargeSmem);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(guard_admit_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem);
+    guard_admit_cta_kernel<<<st->n_segments, kLThreads, smem, (cudaStream_t)stream>>>(*st, *cfg,
+                                                                                      *out);
+    return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+  }
   if (st->n_segments >= plan_group_min()) {
     guard_admit_group_kernel<<<warps_grid((st->n_segments + kPlanGroup - 1) / kPlanGroup, 128), 128, 0,
                                (cudaStream_t)stream>>>(*st, *cfg, *out);

@@ -1,0 +1,589 @@
+// Batched plan_step for FEW, LARGE segments (the config-2 stress shape: one
+// SchedulerState with 32,768 waiting + 32,768 running): one CTA per segment.
+// Included by plan_kernels.cu (same translation unit and helpers).
+//
+// A segment's plan_step is three order-dependent chains -- the TTFT prefix walk
+// over the LDF queue, CPython's compensated sum(1/slo) over the running list
+// (sched_scorpio.py:121), the greedy admission scan (:237-294) -- plus the
+// sum(min_slo/slo) of plan.vbs (:312-315).  One warp walking all of it
+// serially took 2.3 ms at the stress shape.  Here the CTA splits the roles
+// so that the chains overlap and only the unavoidable serial parts stay serial:
+//   walk warps (kLW): tiles of kLTile queue items in walk order; every item that
+//       fails at the tile's incoming prefix is rejected outright in parallel
+//       (prefixes only grow and the estimate is monotone in them), the
+//       survivors are compacted in order to shared memory and warp 0 runs the
+//       exact speculative chain over them alone; statuses / positions by
+//       CTA-wide ballot scans.  A whole-queue certified pass (inflated
+//       any-order prefix bound) first: if nothing can be rejected the queue is
+//       kept as is.
+//   fold warp F0: sum(1/slo) over running, in order (one DADD latency/entry).
+//   aggregate warps F1..F3: min slo and sum of lengths over running; then F1
+//       folds vbs over running with that minimum, speculatively: admission
+//       rarely lowers the minimum, and when it does warp 0 refolds.
+//   warp 0 then runs the admission scan (speculative-parallel rounds, one per
+//       admission per chunk; bookkeeping once per chunk) and finishes vbs over
+//       the admitted entries from F1's fold state.
+// Exactness: every decision and fp64 value comes from the same sequential
+// operations as seg_guard_admit (the reference's order); only independent work
+// moved to other warps.
+
+namespace {
+
+constexpr int kLW = 12;                    // walk warps
+constexpr int kLF = 4;                     // fold / aggregate warps
+constexpr int kLThreads = (kLW + kLF) * 32;
+constexpr int kLWalkThreads = kLW * 32;
+constexpr int kLK = 2;                     // queue items per walk thread per tile
+constexpr int kLTile = kLWalkThreads * kLK;
+constexpr int kLChunks = kLK * kLW;        // warp chunks per tile
+
+// named barriers (0 is __syncthreads)
+constexpr int kBarWalk = 1;   // walk warps
+constexpr int kBarAgg = 2;    // F0 (inv), F1..F3 (min, lens) -> warp 0
+constexpr int kBarRed = 3;    // F1..F3 reduction
+constexpr int kBarVbs = 4;    // F1 (vbs over running) -> warp 0
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Profiling builds only (-DSL_LARGE_PROF): %globaltimer stamps per phase of
+// segment 0, read with sl_large_prof_read: 0 start, 1 walk done, 2 inv fold done,
+// 3 min/lens done, 4 vbs(running) done, 5 admission done, 6 end.
+#ifdef SL_LARGE_PROF
+__device__ unsigned long long sl_large_prof[16];
+#define SL_LCLK(v) (v = clock64())
+#define SL_LSTAMP(k)                                                      \
+  do {                                                                    \
+    if (seg == 0 && lane == 0) {                                          \
+      unsigned long long t_;                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+      sl_large_prof[k] = t_;                                              \
+    }                                                                     \
+  } while (0)
+#else
+#define SL_LSTAMP(k) do {} while (0)
+#define SL_LCLK(v) do {} while (0)
+#endif
+
+struct LargeSmem {
+  double fbuf[2][32];  // fold operand broadcast buffers (F0, F1; 16-byte aligned: first)
+  double sv_e[kLTile], sv_pf[kLTile], sv_tt[kLTile];  // survivors of a tile, in order
+  uint8_t dec[kLTile];                                // chain decision: 1 = rejected
+  int cnt[2][kLChunks];
+  int off[2][kLChunks];
+  double P;        // walk prefix (exact, sequential)
+  double U;        // certified pass: inflated prefix bound
+  int all_ok;
+  int n_sv, kept, nrej, kbase, rbase;
+  // aggregates
+  double inv;      // sum(1/slo) over running (CPython sum, ps_result)
+  double min_pre;  // min slo over running (+inf if none)
+  long long lens;  // sum of current lengths over running
+  double red_min[3];
+  long long red_len[3];
+  PySum vbs_run;   // vbs fold over running with min_pre
+};
+
+// exclusive scan of the kLChunks counts of row r (warp 0), totals to *tot
+__device__ __forceinline__ void chunk_scan(LargeSmem& sm, int r, int lane, int* tot) {
+  static_assert(kLChunks <= 64, "two chunks per lane");
+  const int a = lane < kLChunks ? sm.cnt[r][lane] : 0;
+  const int b = lane + 32 < kLChunks ? sm.cnt[r][lane + 32] : 0;
+  // chunks 0..31 in lanes, then 32..63
+  int x = a;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(SL_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  const int tot_a = __shfl_sync(SL_FULL, x, 31);
+  int z = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(SL_FULL, z, o);
+    if (lane >= o) z += y;
+  }
+  const int tot_b = __shfl_sync(SL_FULL, z, 31);
+  if (lane < kLChunks) sm.off[r][lane] = x - a;
+  if (lane + 32 < kLChunks) sm.off[r][lane + 32] = tot_a + z - b;
+  if (lane == 0) *tot = tot_a + tot_b;
+}
+
+// The sequential walk over the survivors [0, n) in shared memory (warp 0):
+// dec[i] = 1 for rejected; returns the prefix after them.  Rounds of "first
+// item that passes at the current prefix": every item before it fails at this
+// prefix -- rejected, the prefix unchanged -- and it is kept, adding its
+// prefill.  One round per kept item plus one per 64 rejected items, each a
+// lane-parallel test of a 64-item window; exact for any prefill sign.
+__device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double prefix, int lane) {
+  for (int base = 0; base < n; base += 64) {
+    const int j0 = base + lane, j1 = base + 32 + lane;
+    const bool v0 = j0 < n, v1 = j1 < n;
+    double e0 = 0.0, p0 = 0.0, t0 = 0.0, e1 = 0.0, p1 = 0.0, t1 = 0.0;
+    if (v0) {
+      e0 = sm.sv_e[j0];
+      p0 = sm.sv_pf[j0];
+      t0 = sm.sv_tt[j0];
+    }
+    if (v1) {
+      e1 = sm.sv_e[j1];
+      p1 = sm.sv_pf[j1];
+      t1 = sm.sv_tt[j1];
+    }
+    // the window stays in registers; each round retires the lanes up to the
+    // first one that passes at the current prefix
+    bool a0 = v0, a1 = v1, k0 = false, k1 = false;
+    for (;;) {
+      const unsigned ok0 = __ballot_sync(SL_FULL, a0 && !(fadd_(fadd_(e0, prefix), p0) > t0));
+      const unsigned ok1 = __ballot_sync(SL_FULL, a1 && !(fadd_(fadd_(e1, prefix), p1) > t1));
+      if (!(ok0 | ok1)) break;  // every remaining item fails at this prefix
+      const int g = ok0 ? __ffs(ok0) - 1 : 32 + __ffs(ok1) - 1;
+      const double pg = g < 32 ? bcast(p0, g) : bcast(p1, g - 32);
+      k0 |= lane == g;
+      k1 |= lane + 32 == g;
+      a0 &= lane > g;
+      a1 &= lane + 32 > g;
+      prefix = fadd_(prefix, pg);
+    }
+    if (v0) sm.dec[j0] = !k0;
+    if (v1) sm.dec[j1] = !k1;
+  }
+  return prefix;
+}
+
+__device__ __forceinline__ double div_int(int64_t a, int64_t b) {
+  return b <= 128 ? div_small((double)a, (int)b) : fdiv_((double)a, (double)b);
+}
+
+__global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_plan_state st,
+                                                                       const sl_plan_config cfg,
+                                                                       sl_plan_out out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LargeSmem& sm = *reinterpret_cast<LargeSmem*>(smem_raw);
+  const int seg = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const sl_cost& C = cfg.cost;
+  const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
+  const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
+  const bool r_only = cfg.flags & SL_FLAG_R_ONLY;
+  const bool guard_only = cfg.flags & SL_PLAN_GUARD_ONLY;
+  const bool walk = ttft_guard || (cfg.flags & SL_PLAN_FCFS_WALK);
+  const bool exact = cfg.flags & SL_PLAN_EXACT_WALK;
+  const int64_t wb = st.w_begin[seg], rb = st.r_begin[seg];
+  const int W = (int)(st.w_begin[seg + 1] - wb);
+  const int R = (int)(st.r_begin[seg + 1] - rb);
+  const double now = st.now[seg];
+  const int E = st.credit_exp[seg];
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  int32_t* kept_list = out.scratch + wb;
+  const bool need_inv = !guard_only && tpot_guard && R > 0 && W > 0;
+  const bool need_vbs = !guard_only && R > 0;
+  if (tid == 0) SL_LSTAMP(0);
+
+  if (warp >= kLW) {
+    // ------------------------------------------------------------ fold warps
+    if (guard_only) return;  // warp 0 waits on none of their barriers
+    // roles by SMSP (warp % 4): the two long folds off warp 0's SMSP 0
+    static_assert(kLW % 4 == 0 && kLF == 4, "fold warps kLW..kLW+3");
+    const int f = (warp - kLW + 3) & 3;  // warp kLW -> 3 (SMSP 0), kLW+1 -> F0, +2 -> F1, +3 -> 2
+    if (f == 0) {
+      if (need_inv) {  // sum(1.0 / slo) over running, in order (:121)
+        PySum ps;
+        ps_init(ps);
+        double t_n = lane < R ? st.r_tpot[rb + lane] : 1.0;
+        for (int c0 = 0; c0 < R; c0 += 32) {
+          const double x = frcp_(t_n);
+          const int jn = c0 + 32 + lane;
+          t_n = jn < R ? st.r_tpot[rb + jn] : 1.0;
+          ps_add_warp_smem(ps, x, min(32, R - c0), sm.fbuf[0]);
+        }
+        if (lane == 0) sm.inv = ps_result(ps);
+      }
+      SL_LSTAMP(2);
+      bar_arrive(kBarAgg, 5 * 32);
+      return;
+    }
+    // F1..F3: min slo and sum of lengths over running
+    const int ft = (f - 1) * 32 + lane;  // 0..95
+    long long lens = 0;
+    double mn = kInf;
+    for (int j = ft; j < R; j += 96) {
+      lens += st.r_cur_len[rb + j];
+      mn = fmin(mn, st.r_tpot[rb + j]);
+    }
+    lens = warp_sum_i64(lens);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mn = fmin(mn, __shfl_xor_sync(SL_FULL, mn, o));
+    if (lane == 0) {
+      sm.red_min[f - 1] = mn;
+      sm.red_len[f - 1] = lens;
+    }
+    bar_sync(kBarRed, 96);
+    const double min_pre = fmin(fmin(sm.red_min[0], sm.red_min[1]), sm.red_min[2]);
+    if (f == 1 && lane == 0) {
+      sm.min_pre = min_pre;
+      sm.lens = sm.red_len[0] + sm.red_len[1] + sm.red_len[2];
+    }
+    if (f == 1) SL_LSTAMP(3);
+    bar_arrive(kBarAgg, 5 * 32);
+    if (f != 1) return;
+    if (need_vbs) {  // vbs over running with the pre-admission minimum (:312-315)
+      PySum vs;
+      ps_init(vs);
+      double t_n = lane < R ? st.r_tpot[rb + lane] : 1.0;
+      for (int c0 = 0; c0 < R; c0 += 32) {
+        const double x = fdiv_(min_pre, t_n);
+        const int jn = c0 + 32 + lane;
+        t_n = jn < R ? st.r_tpot[rb + jn] : 1.0;
+        ps_add_warp_smem(vs, x, min(32, R - c0), sm.fbuf[1]);
+      }
+      if (lane == 0) sm.vbs_run = vs;
+      SL_LSTAMP(4);
+      bar_arrive(kBarVbs, 2 * 32);  // warp 0 waits on it iff R > 0
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- walk warps
+  if (tid == 0) {
+    sm.P = 0.0;
+    sm.U = 0.0;
+    sm.all_ok = 1;
+    sm.kept = 0;
+    sm.nrej = 0;
+  }
+  bar_sync(kBarWalk, kLWalkThreads);
+  auto qidx = [&](int p) -> int32_t {
+    return ttft_guard ? out.perm[wb + p] : (int32_t)(wb + p);
+  };
+  // certified pass over the whole queue (see seg_guard_admit): an inflated
+  // any-order prefix bound U_j >= the sequential prefix; if every item passes
+  // against it, the walk keeps everything in order.
+  bool certified = !walk;
+  if (walk && !exact && W < (1 << 20)) {
+    const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
+    for (int t0 = 0; t0 < W; t0 += kLTile) {
+      const double U = sm.U;
+      double e[kLK], pf[kLK], tt[kLK], v[kLK];
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < kLK; ++k) {
+        const int p = t0 + k * kLWalkThreads + tid;
+        e[k] = pf[k] = tt[k] = 0.0;
+        if (p < W) {
+          const int32_t idx = qidx(p);
+          e[k] = fsub_(now, st.w_arrival[idx]);
+          pf[k] = st.w_prefill[idx];
+          tt[k] = st.w_ttft[idx];
+        }
+        v[k] = pf[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(SL_FULL, v[k], o);
+          if (lane >= o) v[k] = fadd_(v[k], y);
+        }
+      }
+      // chunk totals -> chunk offsets (any order, inflated below); reuse off[] as doubles
+      double* ctot = reinterpret_cast<double*>(sm.sv_e);
+#pragma unroll
+      for (int k = 0; k < kLK; ++k)
+        if (lane == 31) ctot[k * kLW + warp] = v[k];
+      bar_sync(kBarWalk, kLWalkThreads);
+      if (warp == 0) {
+        double c = 0.0;
+        for (int q = 0; q < kLChunks; ++q) {  // serial, tiny
+          const double x = ctot[q];
+          if (lane == 0) ctot[kLChunks + q] = c;
+          c = fadd_(c, x);
+        }
+        if (lane == 0) ctot[2 * kLChunks] = c;
+      }
+      bar_sync(kBarWalk, kLWalkThreads);
+#pragma unroll
+      for (int k = 0; k < kLK; ++k) {
+        const int p = t0 + k * kLWalkThreads + tid;
+        double excl = __shfl_up_sync(SL_FULL, v[k], 1);
+        if (lane == 0) excl = 0.0;
+        const double Uj = fmul_(fadd_(fmul_(fadd_(U, ctot[kLChunks + k * kLW + warp]), inflate),
+                                      excl), inflate);
+        if (p < W && fadd_(fadd_(e[k], Uj), pf[k]) > tt[k]) ok = false;
+      }
+      const double tile_tot = ctot[2 * kLChunks];
+      if (!__all_sync(SL_FULL, ok)) sm.all_ok = 0;  // benign race: every writer stores 0
+      bar_sync(kBarWalk, kLWalkThreads);
+      if (!sm.all_ok) break;
+      if (tid == 0) sm.U = fmul_(fmul_(fadd_(U, tile_tot), inflate), inflate);
+      bar_sync(kBarWalk, kLWalkThreads);
+    }
+    certified = sm.all_ok != 0;
+  }
+#ifdef SL_LARGE_PROF
+  long long pc[6] = {0, 0, 0, 0, 0, 0}, pt0 = 0, pt1 = 0;
+  long long n_sv_tot = 0;
+#endif
+  if (certified) {
+    for (int p = tid; p < W; p += kLWalkThreads) kept_list[p] = qidx(p);
+    if (tid == 0) sm.kept = W;
+  } else {
+    for (int t0 = 0; t0 < W; t0 += kLTile) {
+      SL_LCLK(pt0);
+      const double P0 = sm.P;
+      double e[kLK], pf[kLK], tt[kLK];
+      int32_t idx[kLK];
+      bool valid[kLK], rej0[kLK], sv[kLK];
+      int slot[kLK];
+#pragma unroll
+      for (int k = 0; k < kLK; ++k) {
+        const int p = t0 + k * kLWalkThreads + tid;
+        valid[k] = p < W;
+        e[k] = pf[k] = tt[k] = 0.0;
+        idx[k] = 0;
+        if (valid[k]) {
+          idx[k] = qidx(p);
+          e[k] = fsub_(now, st.w_arrival[idx[k]]);
+          pf[k] = st.w_prefill[idx[k]];
+          tt[k] = st.w_ttft[idx[k]];
+        }
+        // fails at the tile's incoming prefix -> fails at every later one
+        rej0[k] = valid[k] && !exact && fadd_(fadd_(e[k], P0), pf[k]) > tt[k];
+        sv[k] = valid[k] && !rej0[k];
+        const unsigned m = __ballot_sync(SL_FULL, sv[k]);
+        slot[k] = __popc(m & lanemask_lt());
+        if (lane == 0) sm.cnt[0][k * kLW + warp] = __popc(m);
+      }
+      bar_sync(kBarWalk, kLWalkThreads);
+#ifdef SL_LARGE_PROF
+      SL_LCLK(pt1); pc[0] += pt1 - pt0; pt0 = pt1;
+#endif
+      if (warp == 0) chunk_scan(sm, 0, lane, &sm.n_sv);
+      bar_sync(kBarWalk, kLWalkThreads);
+#pragma unroll
+      for (int k = 0; k < kLK; ++k) {
+        if (sv[k]) {
+          slot[k] += sm.off[0][k * kLW + warp];
+          sm.sv_e[slot[k]] = e[k];
+          sm.sv_pf[slot[k]] = pf[k];
+          sm.sv_tt[slot[k]] = tt[k];
+        }
+      }
+      bar_sync(kBarWalk, kLWalkThreads);
+#ifdef SL_LARGE_PROF
+      SL_LCLK(pt1); pc[1] += pt1 - pt0; pt0 = pt1; n_sv_tot += sm.n_sv;
+#endif
+      if (warp == 0) {
+        const double P1 = survivor_chain(sm, sm.n_sv, P0, lane);
+        if (lane == 0) sm.P = P1;
+      }
+      bar_sync(kBarWalk, kLWalkThreads);
+#ifdef SL_LARGE_PROF
+      SL_LCLK(pt1); pc[2] += pt1 - pt0; pt0 = pt1;
+#endif
+      bool keep[kLK], rj[kLK];
+      int kr[kLK], rr[kLK];
+#pragma unroll
+      for (int k = 0; k < kLK; ++k) {
+        rj[k] = rej0[k] || (sv[k] && sm.dec[slot[k]]);
+        keep[k] = valid[k] && !rj[k];
+        const unsigned mk = __ballot_sync(SL_FULL, keep[k]);
+        const unsigned mr = __ballot_sync(SL_FULL, rj[k]);
+        kr[k] = __popc(mk & lanemask_lt());
+        rr[k] = __popc(mr & lanemask_lt());
+        if (lane == 0) {
+          sm.cnt[0][k * kLW + warp] = __popc(mk);
+          sm.cnt[1][k * kLW + warp] = __popc(mr);
+        }
+      }
+      bar_sync(kBarWalk, kLWalkThreads);
+      if (warp == 0) {
+        int tk, tr;
+        chunk_scan(sm, 0, lane, &tk);
+        chunk_scan(sm, 1, lane, &tr);
+        if (lane == 0) {
+          sm.kbase = sm.kept;
+          sm.rbase = sm.nrej;
+          sm.kept += tk;
+          sm.nrej += tr;
+        }
+      }
+      bar_sync(kBarWalk, kLWalkThreads);
+      const int kbase = sm.kbase, rbase = sm.rbase;
+#pragma unroll
+      for (int k = 0; k < kLK; ++k) {
+        if (keep[k]) kept_list[kbase + sm.off[0][k * kLW + warp] + kr[k]] = idx[k];
+        if (rj[k]) {
+          out.w_status[idx[k]] = SL_PLAN_REJECTED_TTFT;
+          out.w_pos[idx[k]] = rbase + sm.off[1][k * kLW + warp] + rr[k];
+        }
+      }
+      bar_sync(kBarWalk, kLWalkThreads);
+#ifdef SL_LARGE_PROF
+      SL_LCLK(pt1); pc[3] += pt1 - pt0; pt0 = pt1;
+#endif
+    }
+  }
+#ifdef SL_LARGE_PROF
+  if (seg == 0 && tid == 0) {
+    for (int q = 0; q < 4; ++q) sl_large_prof[8 + q] = pc[q];
+    sl_large_prof[12] = n_sv_tot;
+  }
+#endif
+  bar_sync(kBarWalk, kLWalkThreads);
+  const int kept = sm.kept;
+  int nrej = sm.nrej;
+  if (warp == 0) SL_LSTAMP(1);
+  if (guard_only) {
+    for (int p = tid; p < kept; p += kLWalkThreads) {
+      out.w_status[kept_list[p]] = SL_PLAN_WAITING;
+      out.w_pos[kept_list[p]] = p;
+    }
+    if (tid == 0) {
+      out.seg_counts[4 * seg + 0] = kept;
+      out.seg_counts[4 * seg + 1] = 0;
+      out.seg_counts[4 * seg + 2] = nrej;
+    }
+    return;
+  }
+  if (warp != 0) return;
+
+  // ---------------------------------------------------- admission (warp 0)
+  bar_sync(kBarAgg, 5 * 32);
+  int64_t lens = sm.lens;
+  double min_d = sm.min_pre;
+  const double min_pre = min_d;
+  bool has_min = R > 0;
+  int nadm = 0, nwait = 0;
+  int32_t* adm = out.adm_order + wb;
+  if (tpot_guard) {
+    double inv = need_inv ? sm.inv : 0.0;
+    int64_t n_run = R;
+    for (int c0 = 0; c0 < kept; c0 += 32) {
+      const int p = c0 + lane;
+      const bool valid = p < kept;
+      int32_t idx = 0, ln = 0, pred = 0;
+      double tp = 1.0, ic = 0.0;
+      if (valid) {
+        idx = kept_list[p];
+        tp = st.w_tpot[idx];
+        ic = frcp_(tp);
+        ln = st.w_prompt[idx];
+        pred = st.w_pred[idx];
+      }
+      const bool solo = solo_ok(C, tp, ic, ln, pred);  // feasible alone (:279-289)
+      const unsigned vmask = __ballot_sync(SL_FULL, valid);
+      unsigned pend = vmask, admm = 0;
+      // one round per admission: every pending candidate against the same state
+      while (pend) {
+        const bool lt = !has_min || tp < min_d;
+        const double minp = lt ? tp : min_d;
+        const double V = fmul_(minp, fadd_(inv, ic));
+        const double L = div_int(lens + ln, n_run + 1);
+        const double est = tpot_estimate(C, V, L, pred);
+        const double thr = (r_only && has_min) ? min_d : minp;
+        const unsigned okm = __ballot_sync(SL_FULL, ((pend >> lane) & 1u) && est <= thr);
+        if (!okm) break;
+        const int g = __ffs(okm) - 1;
+        if (lane == g && out.w_rec) {
+          double* r5 = out.w_rec + 5 * (int64_t)idx;
+          r5[0] = V;
+          r5[1] = L;
+          r5[2] = minp;
+          r5[3] = est;
+          r5[4] = thr;
+        }
+        admm |= 1u << g;
+        pend &= ~((2u << g) - 1u);  // lanes before g failed against this state; g admitted
+        const double tp_g = bcast(tp, g);
+        n_run += 1;
+        inv = fadd_(inv, bcast(ic, g));  // :275
+        lens += bcast(ln, g);
+        if (!has_min || tp_g < min_d) min_d = tp_g;
+        has_min = true;
+      }
+      // bookkeeping once per chunk: admitted in lane order, the rest failed
+      const unsigned fail = vmask & ~admm;
+      const unsigned keepm = __ballot_sync(SL_FULL, ((fail >> lane) & 1u) && solo);
+      const unsigned rejm = fail & ~keepm;
+      if ((admm >> lane) & 1u) {
+        const int q = nadm + __popc(admm & lanemask_lt());
+        out.w_status[idx] = SL_PLAN_ADMITTED;
+        out.w_pos[idx] = q;
+        adm[q] = idx;
+      } else if ((keepm >> lane) & 1u) {
+        out.w_status[idx] = SL_PLAN_WAITING;
+        out.w_pos[idx] = nwait + __popc(keepm & lanemask_lt());
+      } else if ((rejm >> lane) & 1u) {
+        out.w_status[idx] = SL_PLAN_REJECTED_ADMISSION;
+        out.w_pos[idx] = nrej + __popc(rejm & lanemask_lt());
+      }
+      nadm += __popc(admm);
+      nwait += __popc(keepm);
+      nrej += __popc(rejm);
+    }
+  } else {  // admit everything in queue order (:295-304)
+    for (int p = lane; p < kept; p += 32) {
+      const int32_t idx = kept_list[p];
+      out.w_status[idx] = SL_PLAN_ADMITTED;
+      out.w_pos[idx] = p;
+      adm[p] = idx;
+    }
+    for (int c0 = 0; c0 < kept; c0 += 32) {
+      const int p = c0 + lane;
+      double v = p < kept ? st.w_tpot[kept_list[p]] : min_d;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(SL_FULL, v, o));
+      min_d = fmin(min_d, v);
+    }
+    has_min = has_min || kept > 0;
+    nadm = kept;
+  }
+  __syncwarp();
+  SL_LSTAMP(5);
+
+  // plan.min_slo / plan.vbs over running + admitted, in order (:312-315)
+  double vbs = 0.0;
+  if (has_min) {
+    PySum vs;
+    int j0 = 0;  // first entry (running then admitted) still to fold
+    if (R > 0) bar_sync(kBarVbs, 2 * 32);
+    if (R > 0 && min_d == min_pre) {
+      vs = sm.vbs_run;  // F1 folded the running part with this very minimum
+      j0 = R;
+    } else {
+      ps_init(vs);
+    }
+    const int tot = R + nadm;
+    auto slo = [&](int j) {
+      return j < tot ? (j < R ? st.r_tpot[rb + j] : st.w_tpot[adm[j - R]]) : 1.0;
+    };
+    double t_n = slo(j0 + lane);
+    for (int c0 = j0; c0 < tot; c0 += 32) {
+      const double x = fdiv_(min_d, t_n);
+      t_n = slo(c0 + 32 + lane);
+      ps_add_warp_smem(vs, x, min(32, tot - c0), sm.fbuf[0]);  // F0 is done
+    }
+    vbs = ps_result(vs);
+  }
+  if (lane == 0) {
+    out.seg_counts[4 * seg + 0] = nwait;
+    out.seg_counts[4 * seg + 1] = nadm;
+    out.seg_counts[4 * seg + 2] = nrej;
+    out.seg_vbs[seg] = vbs;
+    out.seg_min_slo[seg] = has_min ? min_d : __longlong_as_double(0x7ff8000000000000LL);
+    out.seg_min_fixed[seg] = has_min ? slo_fixed<false>(min_d, E) : ~0ull;
+  }
+  SL_LSTAMP(6);
+}
+
+}  // namespace
+
+#ifdef SL_LARGE_PROF
+extern "C" int sl_large_prof_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, sl_large_prof, sizeof(unsigned long long) * 16) == cudaSuccess
+             ? 0
+             : SL_ERR_CUDA;
+}
+#endif

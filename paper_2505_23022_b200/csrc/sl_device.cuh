@@ -85,6 +85,55 @@ __device__ __forceinline__ void ps_add_warp(PySum& s, double x, int cnt) {
   }
 }
 
+// ps_add for a sum that already holds a float (s.n > 0): branch-free, so an
+// unrolled run of these keeps only the t = f + x dependency on the chain.
+__device__ __forceinline__ void ps_add_nz(PySum& s, double x) {
+  const double t = fadd_(s.f, x);
+  const bool big = fabs(s.f) >= fabs(x);
+  const double hi = big ? s.f : x, lo = big ? x : s.f;
+  s.c = fadd_(s.c, fadd_(fsub_(hi, t), lo));
+  s.f = t;
+}
+
+// Fold the first `cnt` lanes' values of x into s (as ps_add_warp), the full-chunk
+// case unrolled over ps_add_nz: long folds (thousands of entries) run at about
+// one DADD latency per entry.
+__device__ __forceinline__ void ps_add_warp_long(PySum& s, double x, int cnt) {
+  if (cnt == 32 && s.n > 0) {
+    double v[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) v[t] = __shfl_sync(0xffffffffu, x, t);
+#pragma unroll
+    for (int t = 0; t < 32; ++t) ps_add_nz(s, v[t]);
+  } else {
+    for (int t = 0; t < cnt; ++t) ps_add(s, __shfl_sync(0xffffffffu, x, t));
+  }
+}
+
+// As ps_add_warp_long with the operands gathered through a per-warp shared
+// buffer `buf` (32 doubles, 16-byte aligned) as 16 x LDS.128 broadcasts instead
+// of 64 shuffles: the fold is then bound by its own fp64 issue (~19 cycles per
+// entry measured, tools/ubench_fold.cu) instead of shuffle throughput (~27).
+__device__ __forceinline__ void ps_add_warp_smem(PySum& s, double x, int cnt, double* buf) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  buf[lane] = x;
+  __syncwarp();
+  if (cnt == 32 && s.n > 0) {
+    double v[32];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const double2 p = reinterpret_cast<const double2*>(buf)[t];
+      v[2 * t] = p.x;
+      v[2 * t + 1] = p.y;
+    }
+#pragma unroll
+    for (int t = 0; t < 32; ++t) ps_add_nz(s, v[t]);
+  } else {
+    for (int t = 0; t < cnt; ++t) ps_add(s, buf[t]);
+  }
+}
+
 __device__ __forceinline__ double ps_result(const PySum& s) {
   if (s.n == 0) return 0.0;  // int 0; every use adds it to a float
   double f = s.f;

@@ -28,6 +28,15 @@ CASES = [  # (name, segments, W, R, seed, flags)
     ("stress_32768", 1, 32768, 32768, 9, "both"),
     # the shapes bench.py times (config 2): the primary batch exactly ...
     ("bench_primary_1024", 1024, 32, 32, 11, "both"),
+    # few large segments (the one-CTA-per-segment kernels): multi-tile walks with
+    # admissions, the guard ablations, and admissions that lower the running
+    # minimum (R = 3: vbs refolded with the new minimum)
+    ("large_adm_3000x40", 4, 3000, 40, 12, "both"),
+    ("large_r_only", 2, 2500, 2000, 13, "r_only"),
+    ("large_tpot_only", 2, 3000, 3000, 14, "tpot_only"),
+    ("large_ttft_only", 2, 3000, 3000, 15, "ttft_only"),
+    ("large_neither", 1, 2000, 5000, 16, "neither"),
+    ("large_min_drop", 8, 2000, 3, 17, "both"),
 ]
 # ... and 256 segments spread over the bench's 262,144-segment scaled batch
 # (config2_plan_arrays_fast, seed 11): the test runs the whole batch through the
