@@ -41,7 +41,9 @@ constexpr int kLChunks = kLK * kLW;        // warp chunks per tile
 constexpr int kBarWalk = 1;   // walk warps
 constexpr int kBarAgg = 2;    // F0 (inv), F1..F3 (min, lens) -> warp 0
 constexpr int kBarRed = 3;    // F1..F3 reduction
-constexpr int kBarVbs = 4;    // F1 (vbs over running) -> warp 0
+constexpr int kBarVbs = 4;    // vbs pair (fold over running) -> warp 0
+constexpr int kBarInvRing = 5;   // 5..8: inv fold handover (full x2, empty x2)
+constexpr int kBarVbsRing = 9;   // 9..12: vbs fold handover
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -69,8 +71,18 @@ __device__ unsigned long long sl_large_prof[16];
 #define SL_LCLK(v) do {} while (0)
 #endif
 
+// A long CPython sum() split over two warps (split_fold_f / split_fold_c):
+// slot s of the handover ring holds 32 operands and the running float sum
+// before each of them.
+struct SplitRing {
+  double x[2][32];
+  double fb[2][32];
+};
+
 struct LargeSmem {
-  double fbuf[2][32];  // fold operand broadcast buffers (F0, F1; 16-byte aligned: first)
+  SplitRing sf[2];     // inv, vbs (16-byte aligned: first)
+  double ebuf[2][32];  // c-chain operand broadcast buffers
+  double fbuf[32];     // warp 0's fold operand buffer
   double sv_e[kLTile], sv_pf[kLTile], sv_tt[kLTile];  // survivors of a tile, in order
   uint8_t dec[kLTile];                                // chain decision: 1 = rejected
   int cnt[2][kLChunks];
@@ -80,12 +92,12 @@ struct LargeSmem {
   int all_ok;
   int n_sv, kept, nrej, kbase, rbase;
   // aggregates
-  double inv;      // sum(1/slo) over running (CPython sum, ps_result)
+  double inv_f, inv_c;  // sum(1/slo) over running: the float sum and its compensation
+  double vbs_f, vbs_c;  // vbs over running with min_pre
   double min_pre;  // min slo over running (+inf if none)
   long long lens;  // sum of current lengths over running
-  double red_min[3];
-  long long red_len[3];
-  PySum vbs_run;   // vbs fold over running with min_pre
+  double red_min[2];
+  long long red_len[2];
 };
 
 // exclusive scan of the kLChunks counts of row r (warp 0), totals to *tot
@@ -155,6 +167,104 @@ __device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double pr
   return prefix;
 }
 
+// CPython's sum() over n operands (f += x with Neumaier's
+// compensation c), split over two warps so that each serial chain is one DADD
+// per operand.  split_fold_f (warp A) computes the operands lane-parallel and
+// the float chain f, handing each 32-operand chunk to split_fold_c (warp B)
+// with the value of f before every operand; B forms the exact rounding errors
+// lane-parallel (the same FastTwoSum as ps_add) and chains c over them in order.
+// The pair equals ps_add over the operands bit for bit: the first operand's
+// error is exactly 0 (0.0 + x), so c = 0.0 + 0.0 as ps_add leaves it.
+// Handover: a 2-slot ring, named barriers full[s] (A arrives, B syncs) and
+// empty[s] (B arrives, A syncs): barrier ids bar .. bar + 3.
+// The operand of element j is op(src[j]); loads run two chunks ahead and the
+// operand one chunk ahead of the chain (global-load and division latency off it).
+template <class OP>
+__device__ __forceinline__ double split_fold_f(int n, const double* src, OP op, SplitRing& ring,
+                                               int bar, int lane) {
+  double f = 0.0;
+  int k = 0;
+  double x = lane < n ? op(src[lane]) : 0.0;
+  double raw = 32 + lane < n ? src[32 + lane] : 1.0;
+  for (int c0 = 0; c0 < n; c0 += 32, ++k) {
+    const int s = k & 1;
+    const int cnt = min(32, n - c0);
+    const double xn = op(raw);  // next chunk's operand (1.0 past the end: never folded)
+    const int jnn = c0 + 64 + lane;
+    raw = jnn < n ? src[jnn] : 1.0;
+    if (k >= 2) bar_sync(bar + 2 + s, 64);  // B has read chunk k - 2 from slot s
+    ring.x[s][lane] = x;
+    __syncwarp();
+    if (cnt == 32) {
+      double v[32];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const double2 p = reinterpret_cast<const double2*>(ring.x[s])[t];
+        v[2 * t] = p.x;
+        v[2 * t + 1] = p.y;
+      }
+      // one predicated store per element keeps the chain at ~12 cycles per
+      // element (a register array stored after the chain measured ~19)
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if (lane == 0) ring.fb[s][t] = f;
+        f = fadd_(f, v[t]);
+      }
+    } else {
+      double mine = 0.0;
+      for (int t = 0; t < cnt; ++t) {
+        if (lane == t) mine = f;
+        f = fadd_(f, ring.x[s][t]);
+      }
+      ring.fb[s][lane] = mine;
+    }
+    __syncwarp();
+    bar_arrive(bar + s, 64);
+    x = xn;
+  }
+  // balance the empty barriers of the last two chunks
+  for (int q = max(0, k - 2); q < k; ++q) bar_sync(bar + 2 + (q & 1), 64);
+  return f;
+}
+
+__device__ __forceinline__ double split_fold_c(int n, SplitRing& ring, int bar, double* ebuf,
+                                               int lane) {
+  double c = 0.0;
+  int k = 0;
+  for (int c0 = 0; c0 < n; c0 += 32, ++k) {
+    const int s = k & 1;
+    const int cnt = min(32, n - c0);
+    bar_sync(bar + s, 64);
+    double err = 0.0;
+    if (lane < cnt) {
+      const double f = ring.fb[s][lane], x = ring.x[s][lane];
+      const double t = fadd_(f, x);
+      const bool big = fabs(f) >= fabs(x);
+      const double hi = big ? f : x, lo = big ? x : f;
+      err = fadd_(fsub_(hi, t), lo);  // exact: f + x - t
+    }
+    __syncwarp();  // (err depends on both loads: the slot is read)
+    bar_arrive(bar + 2 + s, 64);
+    ebuf[lane] = err;
+    __syncwarp();
+    if (cnt == 32) {
+      double e[32];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const double2 p = reinterpret_cast<const double2*>(ebuf)[t];
+        e[2 * t] = p.x;
+        e[2 * t + 1] = p.y;
+      }
+#pragma unroll
+      for (int t = 0; t < 32; ++t) c = fadd_(c, e[t]);
+    } else {
+      for (int t = 0; t < cnt; ++t) c = fadd_(c, ebuf[t]);
+    }
+    __syncwarp();
+  }
+  return c;
+}
+
 __device__ __forceinline__ double div_int(int64_t a, int64_t b) {
   return b <= 128 ? div_small((double)a, (int)b) : fdiv_((double)a, (double)b);
 }
@@ -187,63 +297,61 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   if (warp >= kLW) {
     // ------------------------------------------------------------ fold warps
     if (guard_only) return;  // warp 0 waits on none of their barriers
-    // roles by SMSP (warp % 4): the two long folds off warp 0's SMSP 0
+    // roles by SMSP (warp % 4); warp 0 (the serial walk) is on SMSP 0:
+    //   kLW+0 (SMSP 0) vbs c-chain, kLW+1 inv f-chain, kLW+2 inv c-chain,
+    //   kLW+3 vbs f-chain; the vbs pair first reduces min slo / lengths
     static_assert(kLW % 4 == 0 && kLF == 4, "fold warps kLW..kLW+3");
-    const int f = (warp - kLW + 3) & 3;  // warp kLW -> 3 (SMSP 0), kLW+1 -> F0, +2 -> F1, +3 -> 2
-    if (f == 0) {
-      if (need_inv) {  // sum(1.0 / slo) over running, in order (:121)
-        PySum ps;
-        ps_init(ps);
-        double t_n = lane < R ? st.r_tpot[rb + lane] : 1.0;
-        for (int c0 = 0; c0 < R; c0 += 32) {
-          const double x = frcp_(t_n);
-          const int jn = c0 + 32 + lane;
-          t_n = jn < R ? st.r_tpot[rb + jn] : 1.0;
-          ps_add_warp_smem(ps, x, min(32, R - c0), sm.fbuf[0]);
+    const int f = warp - kLW;
+    const double* tp = st.r_tpot + rb;
+    if (f == 1 || f == 2) {  // sum(1.0 / slo) over running, in order (:121)
+      if (need_inv) {
+        if (f == 1) {
+          const double fs = split_fold_f(R, tp, [](double t) { return frcp_(t); }, sm.sf[0],
+                                         kBarInvRing, lane);
+          if (lane == 0) sm.inv_f = fs;
+        } else {
+          const double cs = split_fold_c(R, sm.sf[0], kBarInvRing, sm.ebuf[0], lane);
+          if (lane == 0) sm.inv_c = cs;
         }
-        if (lane == 0) sm.inv = ps_result(ps);
       }
-      SL_LSTAMP(2);
+      if (f == 1) SL_LSTAMP(2);
       bar_arrive(kBarAgg, 5 * 32);
       return;
     }
-    // F1..F3: min slo and sum of lengths over running
-    const int ft = (f - 1) * 32 + lane;  // 0..95
+    // vbs pair: min slo and sum of lengths over running
+    const int ft = (f == 0 ? 0 : 32) + lane;  // 0..63
     long long lens = 0;
     double mn = kInf;
-    for (int j = ft; j < R; j += 96) {
+    for (int j = ft; j < R; j += 64) {
       lens += st.r_cur_len[rb + j];
-      mn = fmin(mn, st.r_tpot[rb + j]);
+      mn = fmin(mn, tp[j]);
     }
     lens = warp_sum_i64(lens);
 #pragma unroll
     for (int o = 16; o; o >>= 1) mn = fmin(mn, __shfl_xor_sync(SL_FULL, mn, o));
     if (lane == 0) {
-      sm.red_min[f - 1] = mn;
-      sm.red_len[f - 1] = lens;
+      sm.red_min[f == 0] = mn;
+      sm.red_len[f == 0] = lens;
     }
-    bar_sync(kBarRed, 96);
-    const double min_pre = fmin(fmin(sm.red_min[0], sm.red_min[1]), sm.red_min[2]);
-    if (f == 1 && lane == 0) {
+    bar_sync(kBarRed, 64);
+    const double min_pre = fmin(sm.red_min[0], sm.red_min[1]);
+    if (f == 3 && lane == 0) {
       sm.min_pre = min_pre;
-      sm.lens = sm.red_len[0] + sm.red_len[1] + sm.red_len[2];
+      sm.lens = sm.red_len[0] + sm.red_len[1];
     }
-    if (f == 1) SL_LSTAMP(3);
+    if (f == 3) SL_LSTAMP(3);
     bar_arrive(kBarAgg, 5 * 32);
-    if (f != 1) return;
     if (need_vbs) {  // vbs over running with the pre-admission minimum (:312-315)
-      PySum vs;
-      ps_init(vs);
-      double t_n = lane < R ? st.r_tpot[rb + lane] : 1.0;
-      for (int c0 = 0; c0 < R; c0 += 32) {
-        const double x = fdiv_(min_pre, t_n);
-        const int jn = c0 + 32 + lane;
-        t_n = jn < R ? st.r_tpot[rb + jn] : 1.0;
-        ps_add_warp_smem(vs, x, min(32, R - c0), sm.fbuf[1]);
+      if (f == 3) {
+        const double fs = split_fold_f(R, tp, [&](double t) { return fdiv_(min_pre, t); },
+                                       sm.sf[1], kBarVbsRing, lane);
+        if (lane == 0) sm.vbs_f = fs;
+        SL_LSTAMP(4);
+      } else {
+        const double cs = split_fold_c(R, sm.sf[1], kBarVbsRing, sm.ebuf[1], lane);
+        if (lane == 0) sm.vbs_c = cs;
       }
-      if (lane == 0) sm.vbs_run = vs;
-      SL_LSTAMP(4);
-      bar_arrive(kBarVbs, 2 * 32);  // warp 0 waits on it iff R > 0
+      bar_arrive(kBarVbs, 3 * 32);  // warp 0 waits on it iff R > 0
     }
     return;
   }
@@ -458,7 +566,11 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   int nadm = 0, nwait = 0;
   int32_t* adm = out.adm_order + wb;
   if (tpot_guard) {
-    double inv = need_inv ? sm.inv : 0.0;
+    double inv = 0.0;
+    if (need_inv) {  // ps_result of the split fold (R > 0 operands)
+      const PySum ps = {sm.inv_f, sm.inv_c, 1};
+      inv = ps_result(ps);
+    }
     int64_t n_run = R;
     for (int c0 = 0; c0 < kept; c0 += 32) {
       const int p = c0 + lane;
@@ -548,9 +660,9 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   if (has_min) {
     PySum vs;
     int j0 = 0;  // first entry (running then admitted) still to fold
-    if (R > 0) bar_sync(kBarVbs, 2 * 32);
+    if (R > 0) bar_sync(kBarVbs, 3 * 32);
     if (R > 0 && min_d == min_pre) {
-      vs = sm.vbs_run;  // F1 folded the running part with this very minimum
+      vs = {sm.vbs_f, sm.vbs_c, 1};  // the vbs pair folded the running part with this minimum
       j0 = R;
     } else {
       ps_init(vs);
@@ -563,7 +675,7 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     for (int c0 = j0; c0 < tot; c0 += 32) {
       const double x = fdiv_(min_d, t_n);
       t_n = slo(c0 + 32 + lane);
-      ps_add_warp_smem(vs, x, min(32, tot - c0), sm.fbuf[0]);  // F0 is done
+      ps_add_warp_smem(vs, x, min(32, tot - c0), sm.fbuf);
     }
     vbs = ps_result(vs);
   }
