@@ -12,6 +12,7 @@
 //  select -- one warp per segment: fixed-point credit earn/debit with ballot
 //            batch compaction (sched_scorpio.py:161-180), or decode-all.
 // All fp64 on the decision path uses the unfused *_rn intrinsics (sl_device.cuh).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -754,6 +755,287 @@ __global__ void __launch_bounds__(kSelCta) credit_select_cta_kernel(const sl_pla
 // Segment count below which credit select runs one CTA per segment.
 constexpr int kSelCtaMaxSegments = 64;
 
+// ---- plan_step of one segment with <= 32 waiting and <= 32 running, all in
+// registers (the config-2 primary shape).  Every input of the segment is loaded
+// up front -- one memory latency instead of one per stage -- and the stages
+// exchange values by shuffles: LDF sort (packed-key network, full-key network on
+// near-ties), TTFT walk (certified any-order bound, else rounds of "first item
+// that passes at the current prefix"), sum(1/slo), admission rounds, vbs, and
+// the credit phase.  Same decisions and fp64 values as seg_sort_warp +
+// seg_guard_admit + seg_credit_select (sched_scorpio.py:117-207, 210-316).
+__device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl_plan_config& cfg,
+                                               const sl_plan_out& out, int seg, int lane,
+                                               double* buf) {
+  const sl_cost& C = cfg.cost;
+  const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
+  const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
+  const bool r_only = cfg.flags & SL_FLAG_R_ONLY;
+  const bool guard_only = cfg.flags & SL_PLAN_GUARD_ONLY;
+  const bool walk = ttft_guard || (cfg.flags & SL_PLAN_FCFS_WALK);
+  const bool exact = cfg.flags & SL_PLAN_EXACT_WALK;
+  const int64_t wb = st.w_begin[seg], rb = st.r_begin[seg];
+  const int W = (int)(st.w_begin[seg + 1] - wb);
+  const int R = (int)(st.r_begin[seg + 1] - rb);
+  const double now = st.now[seg];
+  const int E = st.credit_exp[seg];
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  // ---- every input at once
+  const bool wv = lane < W, rv = lane < R;
+  double arr = 0.0, tt0 = 0.0, pf0 = 0.0, tp0 = 1.0;
+  int32_t pr0 = 0, pd0 = 0;
+  int64_t id0 = 0;
+  if (wv) {
+    arr = st.w_arrival[wb + lane];
+    tt0 = st.w_ttft[wb + lane];
+    pf0 = st.w_prefill[wb + lane];
+    tp0 = st.w_tpot[wb + lane];
+    pr0 = st.w_prompt[wb + lane];
+    pd0 = st.w_pred[wb + lane];
+    id0 = st.w_id[wb + lane];
+  }
+  double rt = 1.0;
+  int32_t rlen = 0;
+  uint64_t rcred = 0;
+  bool rex = false;
+  if (rv) {
+    rt = st.r_tpot[rb + lane];
+    rlen = st.r_cur_len[rb + lane];
+    rcred = st.r_credit[rb + lane];
+    rex = st.r_exclude && st.r_exclude[rb + lane];
+  }
+  // ---- LDF order (sched_scorpio.py:193): src = input position at walk position lane
+  int src = lane;
+  if (ttft_guard) {
+    const double d = wv ? fadd_(arr, tt0) : 0.0;  // core.py:50-53
+    bool done = false;
+    if (__all_sync(SL_FULL, !wv || d >= 0.0)) {
+      uint64_t key = wv ? (((uint64_t)__double_as_longlong(d) & ~31ull) | (uint64_t)lane) : ~0ull;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+          const uint64_t ok = __shfl_xor_sync(SL_FULL, key, j);
+          const bool up = (lane & size) == 0;
+          const bool lower = (lane & j) == 0;
+          key = ((lower == up) == (ok < key)) ? ok : key;
+        }
+      }
+      const uint64_t next = __shfl_down_sync(SL_FULL, key, 1);
+      if (!__any_sync(SL_FULL, lane + 1 < W && (next >> 5) == (key >> 5))) {
+        src = (int)(key & 31);
+        done = true;
+      }
+    }
+    if (!done) {  // ties / near-ties: the full (deadline, arrival, id) network
+      Key k;
+      if (wv) {
+        k.d = d;
+        k.a = arr;
+        k.id = id0;
+        k.idx = lane;
+      } else {
+        k = inf_key();
+      }
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+          Key o;
+          o.d = __shfl_xor_sync(SL_FULL, k.d, j);
+          o.a = __shfl_xor_sync(SL_FULL, k.a, j);
+          o.id = __shfl_xor_sync(SL_FULL, k.id, j);
+          o.idx = __shfl_xor_sync(SL_FULL, k.idx, j);
+          const bool up = (lane & size) == 0;
+          const bool lower = (lane & j) == 0;
+          const bool take = (lower == up) ? key_lt(o, k) : key_lt(k, o);
+          if (take) k = o;
+        }
+      }
+      src = k.idx < 0 ? lane : k.idx;
+    }
+    if (wv) out.perm[wb + lane] = (int32_t)(wb + src);
+  }
+  // fields in walk order
+  const double e = __shfl_sync(SL_FULL, fsub_(now, arr), src);
+  const double pf = __shfl_sync(SL_FULL, pf0, src);
+  const double tt = __shfl_sync(SL_FULL, tt0, src);
+  const double tp = __shfl_sync(SL_FULL, tp0, src);
+  const int32_t ln = __shfl_sync(SL_FULL, pr0, src);
+  const int32_t pred = __shfl_sync(SL_FULL, pd0, src);
+  const int32_t idx = (int32_t)(wb + src);
+  const unsigned vmask = __ballot_sync(SL_FULL, wv);
+
+  // ---- TTFT walk (:196-205)
+  unsigned kept = vmask;
+  if (walk) {
+    bool certified = false;
+    if (!exact) {  // any-order inflated prefix bound (see seg_guard_admit)
+      const double inflate = 1.0 + 9.313225746154785e-10;  // 1 + 2^-30
+      double v = wv ? pf : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(SL_FULL, v, o);
+        if (lane >= o) v = fadd_(v, y);
+      }
+      double excl = __shfl_up_sync(SL_FULL, v, 1);
+      if (lane == 0) excl = 0.0;
+      const double Uj = fmul_(fadd_(0.0, excl), inflate);
+      certified = __all_sync(SL_FULL, !wv || fadd_(fadd_(e, Uj), pf) <= tt);
+    }
+    if (!certified) {  // exact: rounds of the first item passing at the current prefix
+      unsigned alive = vmask;
+      kept = 0;
+      double prefix = 0.0;
+      for (;;) {
+        const unsigned okm =
+            __ballot_sync(SL_FULL, ((alive >> lane) & 1u) && !(fadd_(fadd_(e, prefix), pf) > tt));
+        if (!okm) break;
+        const int g = __ffs(okm) - 1;
+        kept |= 1u << g;
+        alive &= ~((2u << g) - 1u);
+        prefix = fadd_(prefix, bcast(pf, g));
+      }
+    }
+  }
+  const unsigned rejw = vmask & ~kept;
+  if ((rejw >> lane) & 1u) {
+    out.w_status[idx] = SL_PLAN_REJECTED_TTFT;
+    out.w_pos[idx] = __popc(rejw & lanemask_lt());
+  }
+  int nrej = __popc(rejw);
+  if (guard_only) {
+    if ((kept >> lane) & 1u) {
+      out.w_status[idx] = SL_PLAN_WAITING;
+      out.w_pos[idx] = __popc(kept & lanemask_lt());
+    }
+    if (lane == 0) {
+      out.seg_counts[4 * seg + 0] = __popc(kept);
+      out.seg_counts[4 * seg + 1] = 0;
+      out.seg_counts[4 * seg + 2] = nrej;
+    }
+    return;
+  }
+
+  // ---- running aggregates (:117-124)
+  int64_t lens = warp_sum_i64(rv ? (int64_t)rlen : 0);
+  double min_d = rv ? rt : kInf;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) min_d = fmin(min_d, __shfl_xor_sync(SL_FULL, min_d, o));
+  bool has_min = R > 0;
+  unsigned admm = 0, keepm = 0, rejm = 0;
+  if (tpot_guard) {
+    double inv = 0.0;
+    if (kept && R > 0) {
+      PySum ps;
+      ps_init(ps);
+      ps_add_warp_smem(ps, frcp_(rt), R, buf);
+      inv = ps_result(ps);
+    }
+    // ---- admission rounds (:237-294): every pending candidate against one state
+    const double ic = frcp_(tp);
+    const bool solo = solo_ok(C, tp, ic, ln, pred);
+    int64_t n_run = R;
+    unsigned pend = kept;
+    while (pend) {
+      const bool lt = !has_min || tp < min_d;
+      const double minp = lt ? tp : min_d;
+      const double V = fmul_(minp, fadd_(inv, ic));
+      const double L = div_small((double)(lens + ln), (int)(n_run + 1));  // n_run + 1 <= 65
+      const double est = tpot_estimate(C, V, L, pred);
+      const double thr = (r_only && has_min) ? min_d : minp;
+      const unsigned okm = __ballot_sync(SL_FULL, ((pend >> lane) & 1u) && est <= thr);
+      if (!okm) break;
+      const int g = __ffs(okm) - 1;
+      if (lane == g && out.w_rec) {
+        double* r5 = out.w_rec + 5 * (int64_t)idx;
+        r5[0] = V;
+        r5[1] = L;
+        r5[2] = minp;
+        r5[3] = est;
+        r5[4] = thr;
+      }
+      admm |= 1u << g;
+      pend &= ~((2u << g) - 1u);
+      const double tp_g = bcast(tp, g);
+      n_run += 1;
+      inv = fadd_(inv, bcast(ic, g));  // :275
+      lens += bcast(ln, g);
+      if (!has_min || tp_g < min_d) min_d = tp_g;
+      has_min = true;
+    }
+    const unsigned fail = kept & ~admm;
+    keepm = __ballot_sync(SL_FULL, ((fail >> lane) & 1u) && solo);
+    rejm = fail & ~keepm;
+  } else {  // admit everything in queue order (:295-304)
+    admm = kept;
+    double v = (kept >> lane) & 1u ? tp : kInf;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(SL_FULL, v, o));
+    min_d = fmin(min_d, v);
+    has_min = has_min || kept != 0;
+  }
+  const int nadm = __popc(admm);
+  if ((admm >> lane) & 1u) {
+    const int q = __popc(admm & lanemask_lt());
+    out.w_status[idx] = SL_PLAN_ADMITTED;
+    out.w_pos[idx] = q;
+    out.adm_order[wb + q] = idx;
+  } else if ((keepm >> lane) & 1u) {
+    out.w_status[idx] = SL_PLAN_WAITING;
+    out.w_pos[idx] = __popc(keepm & lanemask_lt());
+  } else if ((rejm >> lane) & 1u) {
+    out.w_status[idx] = SL_PLAN_REJECTED_ADMISSION;
+    out.w_pos[idx] = nrej + __popc(rejm & lanemask_lt());
+  }
+  nrej += __popc(rejm);
+
+  // ---- plan.min_slo / plan.vbs over running + admitted, in order (:312-315)
+  double vbs = 0.0;
+  if (has_min) {
+    PySum vs;
+    ps_init(vs);
+    if (R > 0) ps_add_warp_smem(vs, fdiv_(min_d, rt), R, buf);
+    if (nadm) {
+      const bool a = (admm >> lane) & 1u;
+      const double x = a ? fdiv_(min_d, tp) : 0.0;
+      __syncwarp();
+      if (a) buf[__popc(admm & lanemask_lt())] = x;
+      __syncwarp();
+      for (int t = 0; t < nadm; ++t) ps_add(vs, buf[t]);
+    }
+    vbs = ps_result(vs);
+  }
+  const uint64_t MIN = has_min ? slo_fixed<false>(min_d, E) : ~0ull;
+  if (lane == 0) {
+    out.seg_counts[4 * seg + 0] = __popc(keepm);
+    out.seg_counts[4 * seg + 1] = nadm;
+    out.seg_counts[4 * seg + 2] = nrej;
+    out.seg_vbs[seg] = vbs;
+    out.seg_min_slo[seg] = has_min ? min_d : __longlong_as_double(0x7ff8000000000000LL);
+    out.seg_min_fixed[seg] = MIN;
+  }
+  // ---- credit phase (:161-180) or decode-all
+  bool b = false;
+  uint64_t N = rcred;
+  if (rv && !rex) {
+    if (tpot_guard) {
+      const uint64_t S = slo_fixed<false>(rt, E);
+      N += MIN;
+      b = N >= S;
+      if (b) N -= S;
+    } else {
+      b = true;
+    }
+  }
+  const unsigned bm = __ballot_sync(SL_FULL, b);
+  if (rv) {
+    out.r_credit_out[rb + lane] = N;
+    out.r_batch[rb + lane] = b;
+    out.r_pos[rb + lane] = b ? __popc(bm & lanemask_lt()) : -1;
+  }
+  if (lane == 0) out.seg_counts[4 * seg + 3] = __popc(bm);
+}
+
 // ---- the whole plan_step in one launch (segments of <= 32 waiting items):
 // sort, guard + admission, credit select back to back in one warp; the stages
 // hand over through the segment's own global slices (L1-resident), so inputs
@@ -761,9 +1043,14 @@ constexpr int kSelCtaMaxSegments = 64;
 __global__ void __launch_bounds__(256) plan_fused_kernel(const sl_plan_state st,
                                                          const sl_plan_config cfg,
                                                          sl_plan_out out) {
+  __shared__ __align__(16) double bufs[8][32];
   const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (seg >= st.n_segments) return;
   const int lane = threadIdx.x & 31;
+  if (st.r_begin[seg + 1] - st.r_begin[seg] <= 32) {  // (w <= 32 for every segment here)
+    seg_plan_small(st, cfg, out, seg, lane, bufs[threadIdx.x >> 5]);
+    return;
+  }
   if (cfg.flags & SL_FLAG_TTFT_GUARD) {
     seg_sort_warp(st, out.perm, seg, lane);
     __syncwarp();
@@ -803,6 +1090,14 @@ int plan_group_min() {
   return 8192;
 }
 
+// The fused single-launch plan step for segments of <= 32 waiting, below
+// plan_group_min segments (above it the separate kernels are faster: measured
+// 704 vs 492 us at 262,144 segments); SL_PLAN_FUSED=0 disables it (tests).
+bool plan_fused_on() {
+  const char* e = getenv("SL_PLAN_FUSED");
+  return !(e && e[0] == '0');
+}
+
 // Segment count up to which guard + admission runs one CTA per segment
 // (guard_admit_cta_kernel, plan_large.cuh); SL_PLAN_CTA_MAX overrides it.
 int plan_cta_max() {
@@ -823,6 +1118,25 @@ int sl_ttft_sort_batch(const sl_plan_state* st, int64_t max_w, sl_plan_out* out,
   cudaStream_t s = (cudaStream_t)stream;
   if (max_w <= 32) {
     sort_warp_kernel<<<warps_grid(S, 128), 128, 0, s>>>(*st, out->perm);
+    return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+  }
+  if (S <= plan_cta_max() && max_w <= 8 * kSortLoc) {  // few large segments: one cluster each
+    int P = 128;
+    while (P < max_w) P <<= 1;
+    const int cs = P > kSortLoc ? P / kSortLoc : 1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(S * cs);
+    lc.blockDim = dim3(P / cs / 4);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, sort_cluster_kernel, *st, P, out->perm) != cudaSuccess)
+      return SL_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
   }
   if (!out->scratch) return SL_ERR_ARG;
@@ -901,8 +1215,7 @@ int sl_vbs_batch(int32_t n_segments, const int64_t* r_begin, const double* r_tpo
 int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64_t max_w,
                        sl_plan_out* out, void* stream) {
   if (!st || !cfg || !out) return SL_ERR_ARG;
-  if (max_w <= 32 && st->n_segments < plan_group_min()) {  // fused single launch (small
-                                                           // batches; see plan_group_min)
+  if (max_w <= 32 && st->n_segments < plan_group_min() && plan_fused_on()) {  // one launch
     if (!out->scratch || !out->w_status || !out->w_pos || !out->seg_counts ||
         ((cfg->flags & SL_FLAG_TTFT_GUARD) && !out->perm))
       return SL_ERR_ARG;

@@ -699,3 +699,166 @@ extern "C" int sl_large_prof_read(unsigned long long* out) {
              : SL_ERR_CUDA;
 }
 #endif
+
+// ---- LDF sort of few, large segments (<= 32,768 waiting each): one thread-block
+// cluster per segment, one bitonic network over the cluster's shared memory.
+// Each CTA holds kSortLoc (or fewer) packed keys of the segment's padded array;
+// stages whose partner distance reaches across CTAs exchange through
+// distributed shared memory (the lower-rank CTA of each pair does both sides),
+// with a cluster barrier on either side; every other stage is CTA-local.
+// Key: the deadline's bit pattern (non-negative doubles order like their bits)
+// with its low 15 bits replaced by the item's position, so keys are unique and
+// the network moves 8-byte words.  Comparisons whose top 49 bits tie (equal or
+// near-equal deadlines) are decided by the full (deadline, arrival, id) key --
+// then by position, which is the stable order of list.sort
+// (sched_scorpio.py:193) -- read from global memory; exact for every input.
+namespace {
+
+constexpr int kSortLoc = 4096;      // keys per CTA
+constexpr int kSortCtaThreads = 1024;
+constexpr int kPosBits = 15;        // positions < 32,768
+constexpr uint64_t kPosMask = (1ull << kPosBits) - 1;
+
+// x before y in LDF order (keys of one segment starting at global index wb)
+__device__ __noinline__ bool ldf_before_tie(const sl_plan_state& st, int64_t wb, uint64_t x,
+                                            uint64_t y) {
+  const int64_t i = wb + (int64_t)(x & kPosMask), j = wb + (int64_t)(y & kPosMask);
+  const double ai = st.w_arrival[i], aj = st.w_arrival[j];
+  const double di = fadd_(ai, st.w_ttft[i]), dj = fadd_(aj, st.w_ttft[j]);  // core.py:50-53
+  if (di != dj) return di < dj;
+  if (ai != aj) return ai < aj;
+  const int64_t ii = st.w_id[i], ij = st.w_id[j];
+  if (ii != ij) return ii < ij;
+  return x < y;  // equal sort keys: input order (stable sort)
+}
+
+// x before y in LDF order (keys of one segment starting at global index wb).
+// Padding keys have the top bit set (real deadlines are positive doubles) and
+// order by position among themselves.
+__device__ __forceinline__ bool ldf_before(const sl_plan_state& st, int64_t wb, uint64_t x,
+                                           uint64_t y) {
+  if (((x ^ y) >> kPosBits) != 0 || (x >> 63)) return x < y;
+  return ldf_before_tie(st, wb, x, y);
+}
+
+__device__ __forceinline__ uint64_t ldf_first(const sl_plan_state& st, int64_t wb, uint64_t x,
+                                               uint64_t y, bool take_first) {
+  const bool xb = ldf_before(st, wb, x, y);
+  return (xb == take_first) ? x : y;
+}
+
+// Thread t of a CTA holds local positions 4t..4t+3 in registers.  A stage
+// (size, j) pairs position p with p ^ j; p keeps the earlier key iff
+// ((p & j) == 0) == ((global p & size) == 0).  j = 1, 2: inside the thread;
+// 4 <= j <= 64: the partner thread t ^ (j / 4) of the same warp (shuffles);
+// 128 <= j < n_loc: through shared memory; j >= n_loc: the partner CTA's shared
+// memory (DSMEM, the lower rank does both sides).
+__global__ void __launch_bounds__(kSortCtaThreads) sort_cluster_kernel(const sl_plan_state st,
+                                                                       int P, int32_t* perm) {
+  namespace cg = cooperative_groups;
+  __shared__ uint64_t key[kSortLoc];
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int seg = blockIdx.x / cs;
+  const int n_loc = P / cs;  // power of two, 128 .. kSortLoc; blockDim = n_loc / 4
+  const int64_t wb = st.w_begin[seg];
+  const int W = (int)(st.w_begin[seg + 1] - wb);
+  const int g0 = rank * n_loc;  // this CTA's first global position
+  const int t = threadIdx.x;
+  uint64_t r[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int p = g0 + 4 * t + x;
+    r[x] = ~0ull ^ kPosMask ^ (uint64_t)(p & kPosMask);  // padding: top bit set, unique
+    if (p < W) {
+      const double d = fadd_(st.w_arrival[wb + p], st.w_ttft[wb + p]);  // > 0 (core.py:40-47)
+      r[x] = ((uint64_t)__double_as_longlong(d) & ~kPosMask) | (uint64_t)p;
+    }
+  }
+  bool in_smem = false;
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      if (j >= 128) {
+        if (!in_smem) {
+#pragma unroll
+          for (int x = 0; x < 4; ++x) key[4 * t + x] = r[x];
+          in_smem = true;
+        }
+        if (j >= n_loc) {
+          cl.sync();
+          const int pr = rank ^ (j / n_loc);
+          if (rank < pr) {
+            uint64_t* rk = cl.map_shared_rank(key, pr);
+            for (int i = t; i < n_loc; i += blockDim.x) {
+              const bool up = ((g0 + i) & size) == 0;
+              const uint64_t a = key[i], b = rk[i];
+              const bool ab = ldf_before(st, wb, a, b);
+              if (ab != up) {
+                key[i] = b;
+                rk[i] = a;
+              }
+            }
+          }
+          cl.sync();
+        } else {
+          __syncthreads();
+          for (int q = t; q < n_loc / 2; q += blockDim.x) {
+            const int lo = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+            const bool up = ((g0 + lo) & size) == 0;
+            const uint64_t a = key[lo], b = key[lo + j];
+            const bool ab = ldf_before(st, wb, a, b);
+            if (ab != up) {
+              key[lo] = b;
+              key[lo + j] = a;
+            }
+          }
+          __syncthreads();
+        }
+        continue;
+      }
+      if (in_smem) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) r[x] = key[4 * t + x];
+        in_smem = false;
+      }
+      if (j >= 4) {
+        const int tl = j >> 2;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const int p = 4 * t + x;
+          const uint64_t o = __shfl_xor_sync(SL_FULL, r[x], tl);
+          const bool up = ((g0 + p) & size) == 0, lower = (p & j) == 0;
+          r[x] = ldf_first(st, wb, r[x], o, lower == up);
+        }
+      } else {  // j = 2: (0,2), (1,3); j = 1: (0,1), (2,3) -- static register indices
+        auto ce = [&](uint64_t& a, uint64_t& b, int x) {
+          const bool up = ((g0 + 4 * t + x) & size) == 0;
+          const bool ab = ldf_before(st, wb, a, b);
+          const uint64_t lo = ab == up ? a : b, hi = ab == up ? b : a;
+          a = lo;
+          b = hi;
+        };
+        if (j == 2) {
+          ce(r[0], r[2], 0);
+          ce(r[1], r[3], 1);
+        } else {
+          ce(r[0], r[1], 0);
+          ce(r[2], r[3], 2);
+        }
+      }
+    }
+  }
+  if (in_smem) {
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 4; ++x) r[x] = key[4 * t + x];
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int p = g0 + 4 * t + x;
+    if (p < W) perm[wb + p] = (int32_t)(wb + (int64_t)(r[x] & kPosMask));
+  }
+}
+
+}  // namespace

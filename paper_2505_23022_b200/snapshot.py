@@ -23,7 +23,10 @@ def _prefill(phi, theta, ap, bp, n):
 
 
 def config2_arrays(n_segments: int, w: int, r: int, seed: int, now: float = 10.0,
-                   prefill=ACC_PREFILL) -> dict[str, np.ndarray]:
+                   prefill=ACC_PREFILL, tie_grid: float | None = None) -> dict[str, np.ndarray]:
+    """tie_grid: round waiting arrivals to multiples of this (a power of two) so
+    that deadlines tie exactly, between equal arrivals (then the id decides)
+    and between different ones (a1 + t1 == a2 + t2)."""
     rng = np.random.default_rng(seed)
     S, W, R = n_segments, n_segments * w, n_segments * r
     tier_w = rng.integers(0, 3, W)
@@ -47,6 +50,14 @@ def config2_arrays(n_segments: int, w: int, r: int, seed: int, now: float = 10.0
         "r_k": rng.integers(0, 1000, R),
         "now": np.full(S, now),
     }
+    if tie_grid:
+        a["w_arrival"] = np.round(a["w_arrival"] / tie_grid) * tie_grid
+        # TTFT SLOs off their tier by whole grid steps: equal deadlines then also
+        # come from different arrivals (exact: everything is on the 2^-k grid)
+        a["w_ttft"] = a["w_ttft"] + tie_grid * (np.arange(W) % 4)
+        # ids in descending arrival-independent order, so the id tie-break is
+        # visible (equal (deadline, arrival) pairs order by id, not position)
+        a["w_id"] = a["w_id"][::-1].copy()
     a["w_prefill"] = np.array([_prefill(*prefill, int(n)) for n in a["w_prompt"]])
     # credit numerators: after k phases at the strictest tier, (k * MIN) mod S_e
     E = min(math.frexp(t)[1] for _, t in TIERS) - 53

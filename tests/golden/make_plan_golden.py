@@ -38,6 +38,10 @@ CASES = [  # (name, segments, W, R, seed, flags)
     ("large_neither", 1, 2000, 5000, 16, "neither"),
     ("large_min_drop", 8, 2000, 3, 17, "both"),
 ]
+# deadline ties (arrivals on a 2^-4 s grid, ids reversed): the LDF sort's
+# tie-breaks on every route -- warp network (<= 32), one cluster per segment
+TIES = [("ties_small", 16, 32, 8, 18, "both", 0.0625),
+        ("ties_large", 2, 5000, 50, 19, "both", 0.0625)]
 # ... and 256 segments spread over the bench's 262,144-segment scaled batch
 # (config2_plan_arrays_fast, seed 11): the test runs the whole batch through the
 # same kernels the bench times and compares the sampled segments
@@ -66,10 +70,12 @@ def main() -> None:
             "ttft_only": ScorpioConfig(tpot_guard=False), "tpot_only": ScorpioConfig(ttft_guard=False),
             "neither": ScorpioConfig(False, False)}
     blobs, meta = {}, []
-    jobs = [(name, S, W, R, seed, fl, None) for name, S, W, R, seed, fl in CASES] + SAMPLED
-    for name, S, W, R, seed, fl, n_sample in jobs:
+    jobs = ([(name, S, W, R, seed, fl, None, None) for name, S, W, R, seed, fl in CASES]
+            + [(name, S, W, R, seed, fl, None, tg) for name, S, W, R, seed, fl, tg in TIES]
+            + [j + (None,) for j in SAMPLED])
+    for name, S, W, R, seed, fl, n_sample, tg in jobs:
         if n_sample is None:
-            a = config2_arrays(S, W, R, seed)
+            a = config2_arrays(S, W, R, seed, tie_grid=tg)
             states = states_from_arrays(a, T)
             segs = None
         else:
@@ -98,7 +104,8 @@ def main() -> None:
         blobs[k + "vbs"] = np.array(vbs)
         blobs[k + "min_slo"] = np.array(mins)
         blobs[k + "credit"] = np.array(cred, np.uint64)
-        meta.append(dict(name=name, segments=S, w=W, r=R, seed=seed, flags=fl, sample=segs))
+        meta.append(dict(name=name, segments=S, w=W, r=R, seed=seed, flags=fl, sample=segs,
+                         tie_grid=tg))
         print(name, "admitted", sum(map(len, adm)), "rejected", sum(map(len, rej)),
               "batch", sum(map(len, bat)))
     np.savez_compressed(os.path.join(HERE, "plan.npz"), **blobs)
