@@ -22,6 +22,9 @@ namespace sl {
 
 constexpr int kSlots = 2;
 constexpr int kRunCap = 32 * kSlots;
+#ifndef SL_INV_UNROLL
+#define SL_INV_UNROLL 0  // unrolled branch-free 1/slo fold (measured: 112 -> 118 ms, registers)
+#endif
 #ifndef SL_WALK_SKIP
 #define SL_WALK_SKIP 1  // general steps skip the walk while now < walk_until
 #endif
@@ -110,7 +113,19 @@ __device__ __forceinline__ PySum running_inv_sum(const Sim& s, const Slot<WIDE> 
     // 1.0 / tpot: S * 2^E is tpot exactly, so this is the WRec's inv bit for bit
     if (32 * k + lane < R) bc[lane] = frcp_(fixed_to_double<WIDE>(sl[k].S, s.pow2E));
     __syncwarp();
-    for (int t = 0; t < cnt; ++t) ps_add(ps, bc[t]);
+    if (SL_INV_UNROLL && cnt == 32 && ps.n > 0) {
+      double v[32];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const double2 p = reinterpret_cast<const double2*>(bc)[t];
+        v[2 * t] = p.x;
+        v[2 * t + 1] = p.y;
+      }
+#pragma unroll
+      for (int t = 0; t < 32; ++t) ps_add_nz(ps, v[t]);
+    } else {
+      for (int t = 0; t < cnt; ++t) ps_add(ps, bc[t]);
+    }
     __syncwarp();
   }
   return ps;
@@ -349,38 +364,21 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
     }
     const int32_t pred = ps_ & 0x7fffffff;
     const bool solo = (ps_ & (int32_t)0x80000000) != 0;
-    unsigned pend = __ballot_sync(SL_FULL, valid);
+    const unsigned vmask = __ballot_sync(SL_FULL, valid);
+    unsigned pend = vmask, admm = 0;
+    // one round per admission: every pending candidate against the same state A
+    // (_admission_math :99-114); lanes before the first admit fail against A and
+    // are decided; the chunk's failures are settled once after the rounds
     while (pend) {
-      // every pending candidate against the same state A (_admission_math :99-114)
       bool lt = !has_min || tp < mind;
       double minp = lt ? tp : mind;
       double V = fmul_(minp, fadd_(inv, ic));
       double L = div_small((double)(lens + ln), (int)(n_run + 1));
       double est = tpot_estimate(C, V, L, pred);
       double thr = (r_only && has_min) ? mind : minp;
-      bool ok = ((pend >> lane) & 1u) && est <= thr;
-      unsigned okm = __ballot_sync(SL_FULL, ok);
-      int gl = okm ? __ffs(okm) - 1 : 32;
-      unsigned fail = okm ? (pend & ((1u << gl) - 1u)) : pend;
-      // failures before the first admit: outright reject unless feasible alone
-      bool mf = (fail >> lane) & 1u;
-      bool keep = mf && solo;
-      bool rj = mf && !solo;
-      unsigned km = __ballot_sync(SL_FULL, keep);
-      unsigned rm = __ballot_sync(SL_FULL, rj);
-      if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
-      if (rj) {
-        const int64_t rid = s.id[idx];  // ids / lengths only for decided requests
-        int pos = nrej + __popc(rm & lanemask_lt());
-        acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u + 1u);
-        acc.rej_adm++;
-        if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_ADMISSION;
-        if (lg_rej >= 0 && pos < cap_rej) a.log.rej_ids[lg_rej + pos] = rid * 2 + 1;
-      }
-      kept += __popc(km);
-      nrej += __popc(rm);
-      pend &= ~fail;
+      const unsigned okm = __ballot_sync(SL_FULL, ((pend >> lane) & 1u) && est <= thr);
       if (!okm) break;
+      const int gl = __ffs(okm) - 1;
       // admit candidate gl (warp-uniform state update, :250-278)
       if (R >= kRunCap) {
         ok_cap = false;
@@ -431,10 +429,30 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       ps_add(P, pf_g);
       ++nadm;
       ++R;
-      pend &= ~(1u << gl);
+      admm |= 1u << gl;
+      pend &= ~((2u << gl) - 1u);
     }
-    __syncwarp();
     if (!ok_cap) break;
+    // failures: outright reject unless feasible alone (:279-291), in queue order
+    const unsigned fail = vmask & ~admm;
+    const bool mf = (fail >> lane) & 1u;
+    const bool keep = mf && solo;
+    const bool rj = mf && !solo;
+    const unsigned km = __ballot_sync(SL_FULL, keep);
+    const unsigned rm = fail & ~km;
+    __syncwarp();
+    if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
+    if (rj) {
+      const int64_t rid = s.id[idx];  // ids only for decided requests
+      int pos = nrej + __popc(rm & lanemask_lt());
+      acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u + 1u);
+      acc.rej_adm++;
+      if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_ADMISSION;
+      if (lg_rej >= 0 && pos < cap_rej) a.log.rej_ids[lg_rej + pos] = rid * 2 + 1;
+    }
+    kept += __popc(km);
+    nrej += __popc(rm);
+    __syncwarp();
   }
   W = kept;
   g.lens = lens;

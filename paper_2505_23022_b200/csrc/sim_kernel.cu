@@ -717,7 +717,7 @@ __device__ __forceinline__ bool hot_eligible(const sl_sim& sp) {
 template <bool HOT, bool OUT>
 __global__ void __launch_bounds__(32 * kFastWarps, HOT ? SL_HOT_MIN_BLOCKS : 1) sl_sim_fast_kernel(
     const __grid_constant__ KArgs a) {
-  __shared__ Slot<false> scratch[kFastWarps][kRunCap];
+  __shared__ __align__(16) Slot<false> scratch[kFastWarps][kRunCap];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   Workspace ws = carve(a.ws_base, a.slots);
