@@ -1120,13 +1120,19 @@ int sl_ttft_sort_batch(const sl_plan_state* st, int64_t max_w, sl_plan_out* out,
     sort_warp_kernel<<<warps_grid(S, 128), 128, 0, s>>>(*st, out->perm);
     return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
   }
-  if (S <= plan_cta_max() && max_w <= 8 * kSortLoc) {  // few large segments: one cluster each
-    int P = 128;
-    while (P < max_w) P <<= 1;
-    const int cs = P > kSortLoc ? P / kSortLoc : 1;
+  if (S <= plan_cta_max() && max_w <= kSortMaxCluster * kSortLoc) {  // few large segments
+    const int cs = (int)((max_w + kSortLoc - 1) / kSortLoc);  // one cluster per segment
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(sort_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(sort_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(RadixSmem));
+      attr_set = true;
+    }
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(S * cs);
-    lc.blockDim = dim3(P / cs / 4);
+    lc.blockDim = dim3(kSortCtaThreads);
+    lc.dynamicSmemBytes = sizeof(RadixSmem);
     lc.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1135,7 +1141,7 @@ int sl_ttft_sort_batch(const sl_plan_state* st, int64_t max_w, sl_plan_out* out,
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, sort_cluster_kernel, *st, P, out->perm) != cudaSuccess)
+    if (cudaLaunchKernelEx(&lc, sort_cluster_kernel, *st, out->perm) != cudaSuccess)
       return SL_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
   }

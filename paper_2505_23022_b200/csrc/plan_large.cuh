@@ -66,7 +66,28 @@ __device__ unsigned long long sl_large_prof[16];
       sl_large_prof[k] = t_;                                              \
     }                                                                     \
   } while (0)
+__device__ unsigned long long sl_sort_prof[32];  // sort_cluster_kernel: [0] count, clock64 stamps
+__device__ unsigned long long sl_sort_cta[16][4];  // per CTA: globaltimer after scatter / local sort, big, my_n
+#define SL_CTASTAMP(k, v)                                                        \
+  do {                                                                           \
+    if (threadIdx.x == 0 && blockIdx.x < 16) sl_sort_cta[blockIdx.x][k] = (v);   \
+  } while (0)
+__device__ __forceinline__ unsigned long long sl_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SL_SSTAMP()                                                              \
+  do {                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                   \
+      const unsigned long long k_ = sl_sort_prof[0] + 1;                         \
+      if (k_ < 32) sl_sort_prof[k_] = clock64();                                 \
+      sl_sort_prof[0] = k_;                                                      \
+    }                                                                            \
+  } while (0)
 #else
+#define SL_CTASTAMP(k, v) do {} while (0)
+#define SL_SSTAMP() do {} while (0)
 #define SL_LSTAMP(k) do {} while (0)
 #define SL_LCLK(v) do {} while (0)
 #endif
@@ -693,6 +714,13 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
 }  // namespace
 
 #ifdef SL_LARGE_PROF
+extern "C" int sl_sort_prof_read(unsigned long long* out) {  // and reset; out[32..95]: per CTA
+  static const unsigned long long z[32] = {0};
+  if (cudaMemcpyFromSymbol(out + 32, sl_sort_cta, sizeof(unsigned long long) * 64) != cudaSuccess)
+    return SL_ERR_CUDA;
+  if (cudaMemcpyFromSymbol(out, sl_sort_prof, sizeof(z)) != cudaSuccess) return SL_ERR_CUDA;
+  return cudaMemcpyToSymbol(sl_sort_prof, z, sizeof(z)) == cudaSuccess ? 0 : SL_ERR_CUDA;
+}
 extern "C" int sl_large_prof_read(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, sl_large_prof, sizeof(unsigned long long) * 16) == cudaSuccess
              ? 0
@@ -701,164 +729,646 @@ extern "C" int sl_large_prof_read(unsigned long long* out) {
 #endif
 
 // ---- LDF sort of few, large segments (<= 32,768 waiting each): one thread-block
-// cluster per segment, one bitonic network over the cluster's shared memory.
-// Each CTA holds kSortLoc (or fewer) packed keys of the segment's padded array;
-// stages whose partner distance reaches across CTAs exchange through
-// distributed shared memory (the lower-rank CTA of each pair does both sides),
-// with a cluster barrier on either side; every other stage is CTA-local.
-// Key: the deadline's bit pattern (non-negative doubles order like their bits)
-// with its low 15 bits replaced by the item's position, so keys are unique and
-// the network moves 8-byte words.  Comparisons whose top 49 bits tie (equal or
-// near-equal deadlines) are decided by the full (deadline, arrival, id) key --
-// then by position, which is the stable order of list.sort
-// (sched_scorpio.py:193) -- read from global memory; exact for every input.
+// cluster per segment (up to 16 CTAs of 2,048 input items, 1,024 threads each),
+// radix sorting with 8-bit digits.
+//  Key: the deadline's bit pattern (deadlines are positive doubles, which order
+//  like their bits) with its low 15 bits replaced by the item's position; only
+//  bits 15..63 are sorted on (the input is in position order and every pass is
+//  stable), and only the bits in which some key differs from the first.
+//  1. MSD distribution: every CTA ranks its keys on the top varying digit, the
+//     CTAs' digit histograms are pushed into each other's shared memory
+//     (distributed shared memory stores, one cluster barrier), and each key is
+//     stored straight into the CTA that owns its digit bucket -- CTA c owns the
+//     buckets that start in [2048 c, 2048 (c + 1)), so it holds a contiguous
+//     range of final positions (<= 4,096 keys; one more barrier).
+//  2. Each CTA LSD-sorts its range in shared memory (CTA barriers only).
+//  3. Adjacent sorted keys with equal top 49 bits (equal or near-equal
+//     deadlines; checked across CTA boundaries too) send the whole segment to
+//     the exact path: positions radix-sorted from input order by id, then
+//     arrival, then deadline (order-preserving 64-bit images), i.e. by the full
+//     sort key (deadline, arrival, id) and then position -- the stable order of
+//     list.sort (sched_scorpio.py:193).  A bucket distribution that would
+//     overflow a CTA falls back to cluster-wide LSD passes on the packed keys.
+//  Exact for every input.
 namespace {
 
-constexpr int kSortLoc = 4096;      // keys per CTA
+constexpr int kSortLoc = 2048;       // input items per CTA
+constexpr int kSortCap = 4096;       // items a CTA can own after the MSD distribution
+constexpr int kBucketMax = 64;       // largest local bucket placed by counting
+constexpr int kLocalBins = 2048;     // local buckets per CTA
+constexpr int kSortMaxCluster = 16;  // non-portable cluster size (B200 allows 16)
 constexpr int kSortCtaThreads = 1024;
-constexpr int kPosBits = 15;        // positions < 32,768
+constexpr int kSortWarps = kSortCtaThreads / 32;
+constexpr int kPosBits = 15;         // positions < 32,768
 constexpr uint64_t kPosMask = (1ull << kPosBits) - 1;
 
-// x before y in LDF order (keys of one segment starting at global index wb)
-__device__ __noinline__ bool ldf_before_tie(const sl_plan_state& st, int64_t wb, uint64_t x,
-                                            uint64_t y) {
-  const int64_t i = wb + (int64_t)(x & kPosMask), j = wb + (int64_t)(y & kPosMask);
-  const double ai = st.w_arrival[i], aj = st.w_arrival[j];
-  const double di = fadd_(ai, st.w_ttft[i]), dj = fadd_(aj, st.w_ttft[j]);  // core.py:50-53
-  if (di != dj) return di < dj;
-  if (ai != aj) return ai < aj;
-  const int64_t ii = st.w_id[i], ij = st.w_id[j];
-  if (ii != ij) return ii < ij;
-  return x < y;  // equal sort keys: input order (stable sort)
-}
+struct RadixSmem {
+  uint64_t buf[2][kSortCap];           // items, double-buffered (DSMEM scatter target)
+  uint32_t cnt[257 * kSortWarps];      // per (digit, warp): count, then CTA-local offset
+  uint32_t hall[kSortMaxCluster][256];  // every CTA's digit totals (pushed by each CTA)
+  uint32_t gbase[256];
+  int32_t owner[256];                  // MSD: owning CTA of each digit bucket
+  int32_t bidx[256];                   // MSD: index among this CTA's non-empty buckets
+  int32_t nmine;
+  int32_t start[kSortMaxCluster + 1];  // MSD: first final position owned by each CTA
+  uint32_t wsum[kSortWarps];
+  unsigned long long vall[kSortMaxCluster];  // every CTA's flag word (pushed)
+  unsigned long long tfirst[kSortMaxCluster], tlast[kSortMaxCluster];  // MSD tie check
+  unsigned long long vmin[kSortMaxCluster], vmax[kSortMaxCluster];    // key range exchange
+  uint32_t lh[kLocalBins];             // bucket counts, then offsets (MSD: 256, local: 2048)
+  unsigned long long vary, kmin, kmax;
+};
 
-// x before y in LDF order (keys of one segment starting at global index wb).
-// Padding keys have the top bit set (real deadlines are positive doubles) and
-// order by position among themselves.
-__device__ __forceinline__ bool ldf_before(const sl_plan_state& st, int64_t wb, uint64_t x,
-                                           uint64_t y) {
-  if (((x ^ y) >> kPosBits) != 0 || (x >> 63)) return x < y;
-  return ldf_before_tie(st, wb, x, y);
-}
-
-__device__ __forceinline__ uint64_t ldf_first(const sl_plan_state& st, int64_t wb, uint64_t x,
-                                               uint64_t y, bool take_first) {
-  const bool xb = ldf_before(st, wb, x, y);
-  return (xb == take_first) ? x : y;
-}
-
-// Thread t of a CTA holds local positions 4t..4t+3 in registers.  A stage
-// (size, j) pairs position p with p ^ j; p keeps the earlier key iff
-// ((p & j) == 0) == ((global p & size) == 0).  j = 1, 2: inside the thread;
-// 4 <= j <= 64: the partner thread t ^ (j / 4) of the same warp (shuffles);
-// 128 <= j < n_loc: through shared memory; j >= n_loc: the partner CTA's shared
-// memory (DSMEM, the lower rank does both sides).
-__global__ void __launch_bounds__(kSortCtaThreads) sort_cluster_kernel(const sl_plan_state st,
-                                                                       int P, int32_t* perm) {
+// Cluster-wide minimum and maximum of the valid items (pushed into every CTA,
+// one cluster barrier).
+template <int NS>
+__device__ __forceinline__ void cluster_minmax(RadixSmem& sm, const uint64_t (&v)[NS],
+                                               const bool (&ok)[NS], uint64_t& gmin,
+                                               uint64_t& gmax) {
   namespace cg = cooperative_groups;
-  __shared__ uint64_t key[kSortLoc];
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  if (threadIdx.x == 0) {
+    sm.kmin = ~0ull;
+    sm.kmax = 0;
+  }
+  __syncthreads();
+  uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+  for (int x = 0; x < NS; ++x)
+    if (ok[x]) {
+      mn = min(mn, v[x]);
+      mx = max(mx, v[x]);
+    }
+  if (mn != ~0ull) atomicMin(&sm.kmin, (unsigned long long)mn);
+  if (mx != 0) atomicMax(&sm.kmax, (unsigned long long)mx);
+  __syncthreads();
+  if ((int)threadIdx.x < cs) {
+    cl.map_shared_rank(sm.vmin, (int)threadIdx.x)[rank] = sm.kmin;
+    cl.map_shared_rank(sm.vmax, (int)threadIdx.x)[rank] = sm.kmax;
+  }
+  if (cs > 1) cl.sync(); else __syncthreads();
+  gmin = ~0ull;
+  gmax = 0;
+  for (int q = 0; q < cs; ++q) {
+    gmin = min(gmin, (uint64_t)sm.vmin[q]);
+    gmax = max(gmax, (uint64_t)sm.vmax[q]);
+  }
+}
+
+// Push this CTA's word v into slot `rank` of every CTA's vall[] (DSMEM stores,
+// no round trips), then a cluster barrier; returns the OR over the cluster.
+__device__ __forceinline__ unsigned long long cluster_or(RadixSmem& sm, unsigned long long v) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  if ((int)threadIdx.x < cs) cl.map_shared_rank(sm.vall, (int)threadIdx.x)[rank] = v;
+  if (cs > 1) cl.sync(); else __syncthreads();
+  unsigned long long all = 0;
+  for (int q = 0; q < cs; ++q) all |= sm.vall[q];
+  return all;
+}
+
+__device__ __forceinline__ void cluster_bar() {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  if (cl.num_blocks() > 1) cl.sync(); else __syncthreads();
+}
+
+// Order-preserving unsigned image of a double (-0.0 == 0.0, as Python compares).
+__device__ __forceinline__ uint64_t dbl_ord(double v) {
+  uint64_t u = v == 0.0 ? 0ull : (uint64_t)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | (1ull << 63));
+}
+
+// Exclusive scan of one value per thread over the CTA (1024 threads); returns
+// this thread's exclusive prefix.
+__device__ __forceinline__ uint32_t cta_excl_scan(uint32_t v, uint32_t* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(SL_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(SL_FULL, s, o);
+      if (lane >= o) s += y;
+    }
+    wsum[lane] = s - wsum[lane];  // exclusive over warps
+  }
+  __syncthreads();
+  return wsum[w] + x - v;
+}
+
+// NS items per thread: slot x of warp w holds local position (NS w + x) 32 + lane.
+template <int NS>
+struct RadixItems {
+  uint64_t v[NS];
+  bool ok[NS];
+};
+template <int NS>
+__device__ __forceinline__ int item_pos(int x) {
+  return (NS * (threadIdx.x >> 5) + x) * 32 + (threadIdx.x & 31);
+}
+
+// Counter of (digit d, warp w): warp-major rows padded to 257 words, so the
+// ranking (lanes of one warp, distinct digits) and the scan (8 consecutive warps
+// of a digit per thread) hit distinct banks.
+__device__ __forceinline__ int cidx(int d, int w) { return w * 257 + d; }
+
+// Stable ranks of the items' digits d[] (valid items only): r[x] = number of
+// the warp's earlier items with the same digit (ballot peers; slots in order),
+// and sm.cnt = CTA-local exclusive offsets in (digit, warp) order, so an item's
+// rank in the CTA is cnt[cidx(d, w)] + r.
+template <int NS>
+__device__ __forceinline__ void rank_digits(RadixSmem& sm, const int (&d)[NS],
+                                            const bool (&ok)[NS], uint32_t (&r)[NS]) {
+  const int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 257 * kSortWarps; i += blockDim.x) sm.cnt[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int x = 0; x < NS; ++x) {
+    unsigned peers = __ballot_sync(SL_FULL, ok[x]);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const bool bit = (d[x] >> b) & 1;
+      const unsigned bb = __ballot_sync(SL_FULL, bit);
+      peers &= bit ? bb : ~bb;
+    }
+    const unsigned lt = peers & lanemask_lt();
+    r[x] = ok[x] ? sm.cnt[cidx(d[x], w)] + __popc(lt) : 0u;
+    __syncwarp();
+    if (ok[x] && lt == 0) sm.cnt[cidx(d[x], w)] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive offsets in (digit, warp) order: thread t owns digit t / 4,
+  // warps 8 (t % 4) .. 8 (t % 4) + 7
+  const int sd = threadIdx.x >> 2, sw = (threadIdx.x & 3) * 8;
+  uint32_t c8[8], s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    c8[k] = sm.cnt[cidx(sd, sw + k)];
+    s += c8[k];
+  }
+  uint32_t e = cta_excl_scan(s, sm.wsum);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    sm.cnt[cidx(sd, sw + k)] = e;
+    e += c8[k];
+  }
+  __syncthreads();
+}
+
+// This CTA's total for digit dd (offsets (dd, 0) .. (dd + 1, 0)); n = valid items.
+__device__ __forceinline__ uint32_t digit_total(const RadixSmem& sm, int dd, int n) {
+  const uint32_t hi = dd < 255 ? sm.cnt[cidx(dd + 1, 0)] : (uint32_t)n;
+  return hi - sm.cnt[cidx(dd, 0)];
+}
+
+// Push every digit total into slot `rank` of every CTA's hall[] (thread t:
+// digit t & 255, CTAs t >> 8, + 4, ...), then a cluster barrier; thread t < 256
+// gets the total of digit t over the cluster and over the CTAs before this one.
+__device__ __forceinline__ void exchange_hist(RadixSmem& sm, int n, uint32_t& tot, uint32_t& pre) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int dd = threadIdx.x & 255;
+  const uint32_t h = digit_total(sm, dd, n);
+  for (int q = threadIdx.x >> 8; q < cs; q += kSortCtaThreads / 256)
+    cl.map_shared_rank(&sm.hall[rank][0], q)[dd] = h;
+  cluster_bar();
+  tot = 0;
+  pre = 0;
+  if (threadIdx.x < 256)
+    for (int q = 0; q < cs; ++q) {
+      const uint32_t x = sm.hall[q][threadIdx.x];
+      tot += x;
+      pre += q < rank ? x : 0u;
+    }
+}
+
+// One stable LSD pass over the cluster on digit (IMG(item) >> shift) & 255,
+// items in the input layout (2 per thread, kSortLoc per CTA).
+template <class Img>
+__device__ __forceinline__ void cluster_pass(RadixSmem& sm, RadixItems<2>& it, int& cur,
+                                             int shift, const Img& img, int n_here) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks();
+  const int w = threadIdx.x >> 5;
+  int d[2];
+  uint32_t r[2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) d[x] = it.ok[x] ? (int)((img(it.v[x]) >> shift) & 255u) : 0;
+  rank_digits<2>(sm, d, it.ok, r);
+  uint32_t tot, pre;
+  exchange_hist(sm, n_here, tot, pre);
+  // global base per digit: all CTAs' items of smaller digits + earlier CTAs' items
+  const uint32_t ex = cta_excl_scan(threadIdx.x < 256 ? tot : 0u, sm.wsum);
+  if (threadIdx.x < 256) sm.gbase[threadIdx.x] = ex + pre - sm.cnt[cidx(threadIdx.x, 0)];
+  __syncthreads();
+  uint64_t* dst = sm.buf[cur ^ 1];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    if (!it.ok[x]) continue;
+    const uint32_t pos = sm.gbase[d[x]] + sm.cnt[cidx(d[x], w)] + r[x];
+    if (cs > 1)
+      cl.map_shared_rank(dst, (int)(pos / kSortLoc))[pos % kSortLoc] = it.v[x];
+    else
+      dst[pos] = it.v[x];
+  }
+  cluster_bar();
+  cur ^= 1;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+    if (it.ok[x]) it.v[x] = sm.buf[cur][item_pos<2>(x)];
+}
+
+// One stable LSD pass inside the CTA on digit (item >> shift) & 255.
+template <int NS>
+__device__ __forceinline__ void local_pass(RadixSmem& sm, RadixItems<NS>& it, int& cur,
+                                           int shift) {
+  const int w = threadIdx.x >> 5;
+  int d[NS];
+  uint32_t r[NS];
+#pragma unroll
+  for (int x = 0; x < NS; ++x) d[x] = it.ok[x] ? (int)((it.v[x] >> shift) & 255u) : 0;
+  rank_digits<NS>(sm, d, it.ok, r);
+  uint64_t* dst = sm.buf[cur ^ 1];
+#pragma unroll
+  for (int x = 0; x < NS; ++x)
+    if (it.ok[x]) dst[sm.cnt[cidx(d[x], w)] + r[x]] = it.v[x];
+  __syncthreads();
+  cur ^= 1;
+#pragma unroll
+  for (int x = 0; x < NS; ++x)
+    if (it.ok[x]) it.v[x] = sm.buf[cur][item_pos<NS>(x)];
+}
+
+// Varying bits of IMG over the cluster's items, relative to `ref` (cluster barrier).
+template <class Img>
+__device__ __forceinline__ uint64_t cluster_vary(RadixSmem& sm, const RadixItems<2>& it,
+                                                 uint64_t ref, const Img& img) {
+  uint64_t v = 0;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+    if (it.ok[x]) v |= img(it.v[x]) ^ ref;
+  const unsigned hi = __reduce_or_sync(SL_FULL, (unsigned)(v >> 32));
+  const unsigned lo = __reduce_or_sync(SL_FULL, (unsigned)v);
+  if (threadIdx.x == 0) sm.vary = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && (hi | lo))
+    atomicOr(&sm.vary, ((unsigned long long)hi << 32) | lo);
+  __syncthreads();
+  return cluster_or(sm, sm.vary);
+}
+
+// Cluster LSD sort on the varying bits [lo_bit, 64) of IMG (relative to ref).
+template <class Img>
+__device__ __forceinline__ void cluster_sort_on(RadixSmem& sm, RadixItems<2>& it, int& cur,
+                                                int lo_bit, uint64_t ref, const Img& img,
+                                                int n_here) {
+  const uint64_t all = cluster_vary(sm, it, ref, img) >> lo_bit;
+  const int nbits = all ? 64 - __clzll((long long)all) : 0;
+  SL_SSTAMP();
+  for (int b = 0; b < nbits; b += 8) {
+    cluster_pass(sm, it, cur, lo_bit + b, img, n_here);
+    SL_SSTAMP();
+  }
+  if (nbits == 0) cluster_bar();  // vall read everywhere before it is reused
+}
+
+struct ImgKey {  // fast pass: the packed key itself
+  __device__ __forceinline__ uint64_t operator()(uint64_t k) const { return k; }
+};
+struct ImgId {  // exact pass, items = positions: id as an unsigned image
+  const int64_t* id;
+  __device__ __forceinline__ uint64_t operator()(uint64_t p) const {
+    return (uint64_t)id[p] ^ (1ull << 63);
+  }
+};
+struct ImgArr {
+  const double* arr;
+  __device__ __forceinline__ uint64_t operator()(uint64_t p) const { return dbl_ord(arr[p]); }
+};
+struct ImgDl {
+  const double* arr;
+  const double* ttft;
+  __device__ __forceinline__ uint64_t operator()(uint64_t p) const {
+    return dbl_ord(fadd_(arr[p], ttft[p]));  // Request.deadline, core.py:50-53
+  }
+};
+
+__device__ __forceinline__ uint64_t packed_key(const sl_plan_state& st, int64_t wb, int p) {
+  const double d = fadd_(st.w_arrival[wb + p], st.w_ttft[wb + p]);  // > 0 (core.py:40-47)
+  return ((uint64_t)__double_as_longlong(d) & ~kPosMask) | (uint64_t)p;
+}
+
+// Adjacent sorted keys (x, next) with equal top 49 bits?
+__device__ __forceinline__ bool near_tie(uint64_t x, uint64_t nx) {
+  return ((x ^ nx) >> kPosBits) == 0;
+}
+
+// MSD distribution + CTA-local bucket sort (see above).  Returns false (nothing
+// written, no shared state pending) if some CTA would own more than kSortCap
+// keys.  Otherwise writes the sorted positions to perm unless *tie (near-ties:
+// the caller runs the exact path).  Neither step needs to be stable: keys are
+// unique, and every key's final place is decided by the local sort.
+__device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W, int hb,
+                                         uint64_t gmin, uint64_t gmax, int64_t wb,
+                                         int32_t* perm, bool* tie) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  // 1. bucket = floor(256 (d - dmin) / (dmax - dmin)), clamped: monotone in the
+  // key's deadline d (IEEE subtraction of, and multiplication by, a constant are
+  // monotone); slot inside the CTA's part of the bucket from a shared atomic
+  const double dlo = __longlong_as_double((long long)(gmin & ~kPosMask));
+  const double sc = 256.0 / (__longlong_as_double((long long)(gmax & ~kPosMask)) - dlo);
+  if (threadIdx.x < 256) sm.lh[threadIdx.x] = 0;
+  __syncthreads();
+  int d[2];
+  uint32_t slot[2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const double dk = __longlong_as_double((long long)(in.v[x] & ~kPosMask));
+    d[x] = min(255, (int)((dk - dlo) * sc));
+    if (in.ok[x]) slot[x] = atomicAdd(&sm.lh[d[x]], 1u);
+  }
+  __syncthreads();
+  // push the CTA's bucket totals into slot `rank` of every CTA's hall[]
+  {
+    const int dd = threadIdx.x & 255;
+    const uint32_t h = sm.lh[dd];
+    for (int q = threadIdx.x >> 8; q < cs; q += kSortCtaThreads / 256)
+      cl.map_shared_rank(&sm.hall[rank][0], q)[dd] = h;
+  }
+  cluster_bar();
+  uint32_t tot = 0, pre = 0;
+  if (threadIdx.x < 256)
+    for (int q = 0; q < cs; ++q) {
+      const uint32_t x = sm.hall[q][threadIdx.x];
+      tot += x;
+      pre += q < rank ? x : 0u;
+    }
+  const uint32_t base = cta_excl_scan(threadIdx.x < 256 ? tot : 0u, sm.wsum);
+  if (threadIdx.x <= kSortMaxCluster) sm.start[threadIdx.x] = W;
+  __syncthreads();
+  int own = 0;
+  if (threadIdx.x < 256) {
+    own = (int)(base / kSortLoc);
+    sm.owner[threadIdx.x] = own;
+    if (tot) atomicMin(&sm.start[own], (int)base);
+    sm.gbase[threadIdx.x] = base + pre;  // this CTA's first place in the bucket
+  }
+  // index of each non-empty bucket among the ones this CTA owns (local sub-bucketing)
+  const bool mine = threadIdx.x < 256 && tot > 0 && own == rank;
+  const uint32_t bix = cta_excl_scan(mine ? 1u : 0u, sm.wsum);
+  if (threadIdx.x < 256) sm.bidx[threadIdx.x] = (int)bix;
+  if (threadIdx.x == 255) sm.nmine = (int)bix + (mine ? 1 : 0);
+  __syncthreads();
+  // owned counts (every CTA computes the same table): start of the next owner
+  bool over = false;
+  int my_start = W, my_n = 0;
+  {
+    int nxt = W;
+    for (int c = cs - 1; c >= 0; --c) {
+      const int s0 = sm.start[c];
+      if (s0 < W) {
+        over |= nxt - s0 > kSortCap;
+        if (c == rank) {
+          my_start = s0;
+          my_n = nxt - s0;
+        }
+        nxt = s0;
+      }
+    }
+  }
+  if (over) {
+    cluster_bar();  // hall / start read everywhere before the fallback reuses them
+    return false;
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    if (!in.ok[x]) continue;
+    const int own = sm.owner[d[x]];
+    const int pos = (int)(sm.gbase[d[x]] + slot[x]) - sm.start[own];
+    if (cs > 1)
+      cl.map_shared_rank(sm.buf[0], own)[pos] = in.v[x];
+    else
+      sm.buf[0][pos] = in.v[x];
+  }
+  cluster_bar();
+  SL_SSTAMP();
+  SL_CTASTAMP(0, sl_gtime());
+  SL_CTASTAMP(3, my_n);
+  // 2. CTA-local sort of the owned range: each owned non-empty MSD bucket is cut
+  // into K = kLocalBins / (owned non-empty buckets) sub-buckets by linear
+  // interpolation inside it -- local digit = (bucket index) K + sub-bucket, monotone
+  // in the deadline like the MSD bucket -- with slots by shared atomics; then
+  // each key's place inside its sub-bucket by counting the sub-bucket's smaller
+  // keys.  A sub-bucket of more than kBucketMax keys (clustered deadlines) sends
+  // the CTA to LSD passes on its varying bits instead.
+  RadixItems<4> it;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    it.ok[x] = item_pos<4>(x) < my_n;
+    it.v[x] = it.ok[x] ? sm.buf[0][item_pos<4>(x)] : 0ull;
+  }
+  for (int i = threadIdx.x; i < kLocalBins; i += blockDim.x) sm.lh[i] = 0;
+  __syncthreads();
+  const int K = kLocalBins / max(1, sm.nmine);
+  int ld[4];
+  uint32_t ls[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const double dk = __longlong_as_double((long long)(it.v[x] & ~kPosMask));
+    const double xs = (dk - dlo) * sc;  // the MSD step's value: same bucket
+    const int B = min(255, (int)xs);
+    const int sub = min(K - 1, (int)((xs - (double)B) * (double)K));
+    ld[x] = sm.bidx[B] * K + sub;
+    if (it.ok[x]) ls[x] = atomicAdd(&sm.lh[ld[x]], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of the bucket counts (kLocalBins / blockDim per thread)
+  constexpr int kPer = kLocalBins / kSortCtaThreads;
+  uint32_t hc[kPer], hs = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    hc[k] = sm.lh[kPer * threadIdx.x + k];
+    hs += hc[k];
+  }
+  bool big = false;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) big |= hc[k] > (uint32_t)kBucketMax;
+  uint32_t e = cta_excl_scan(hs, sm.wsum);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    sm.lh[kPer * threadIdx.x + k] = e;
+    e += hc[k];
+  }
+  big = __syncthreads_or(big) != 0;
+  int cur = 0;
+  if (!big) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (it.ok[x]) sm.buf[1][sm.lh[ld[x]] + ls[x]] = it.v[x];
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      if (!it.ok[x]) continue;
+      const int b0 = (int)sm.lh[ld[x]];
+      const int b1 = ld[x] + 1 < kLocalBins ? (int)sm.lh[ld[x] + 1] : my_n;
+      int k = 0;
+      for (int j = b0; j < b1; ++j) k += sm.buf[1][j] < it.v[x];
+      sm.buf[0][b0 + k] = it.v[x];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (it.ok[x]) it.v[x] = sm.buf[0][item_pos<4>(x)];
+  } else {
+    if (threadIdx.x == 0) {
+      sm.kmin = ~0ull;
+      sm.kmax = 0;
+    }
+    __syncthreads();
+    uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (it.ok[x]) {
+        mn = min(mn, it.v[x]);
+        mx = max(mx, it.v[x]);
+      }
+    if (mn != ~0ull) atomicMin(&sm.kmin, (unsigned long long)mn);
+    if (mx != 0) atomicMax(&sm.kmax, (unsigned long long)mx);
+    __syncthreads();
+    const uint64_t lv = (sm.kmin ^ sm.kmax) >> kPosBits;
+    const int lhb = lv ? kPosBits + 63 - __clzll((long long)lv) : kPosBits - 1;
+    for (int b = kPosBits; b <= lhb; b += 8) local_pass<4>(sm, it, cur, b);
+  }
+  SL_SSTAMP();
+  SL_CTASTAMP(1, sl_gtime());
+  SL_CTASTAMP(2, big);
+  // 3. near-tie check inside the range, then across ranges (first / last keys pushed)
+  bool t = false;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int p = item_pos<4>(x);
+    if (it.ok[x] && p + 1 < my_n) t |= near_tie(it.v[x], sm.buf[cur][p + 1]);
+  }
+  t = __syncthreads_or(t) != 0;
+  if ((int)threadIdx.x < cs) {
+    const int q = (int)threadIdx.x;
+    const unsigned long long fl = my_n ? sm.buf[cur][0] : ~0ull;
+    const unsigned long long la = my_n ? sm.buf[cur][my_n - 1] : ~0ull;
+    cl.map_shared_rank(sm.tfirst, q)[rank] = fl;
+    cl.map_shared_rank(sm.tlast, q)[rank] = la;
+  }
+  const bool any = cluster_or(sm, t) != 0;  // its barrier also publishes tfirst / tlast
+  bool bt = false;
+  {
+    unsigned long long prev = ~0ull;  // last key of the previous non-empty range
+    for (int c = 0; c < cs; ++c) {
+      if (sm.tfirst[c] == ~0ull) continue;
+      if (prev != ~0ull) bt |= near_tie(prev, sm.tfirst[c]);
+      prev = sm.tlast[c];
+    }
+  }
+  *tie = any || bt;  // the same in every CTA
+  if (!*tie) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (it.ok[x]) perm[wb + my_start + item_pos<4>(x)] = (int32_t)(wb + (int64_t)(it.v[x] & kPosMask));
+  } else {
+    cluster_bar();  // tfirst / vall read everywhere before the exact path reuses them
+  }
+  return true;  // no DSMEM access is pending: CTAs may exit
+}
+
+__global__ void __launch_bounds__(kSortCtaThreads) sort_cluster_kernel(const sl_plan_state st,
+                                                                       int32_t* perm) {
+  namespace cg = cooperative_groups;
+  extern __shared__ unsigned char sort_smem_raw[];
+  RadixSmem& sm = *reinterpret_cast<RadixSmem*>(sort_smem_raw);
   cg::cluster_group cl = cg::this_cluster();
   const int cs = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
   const int seg = blockIdx.x / cs;
-  const int n_loc = P / cs;  // power of two, 128 .. kSortLoc; blockDim = n_loc / 4
   const int64_t wb = st.w_begin[seg];
   const int W = (int)(st.w_begin[seg + 1] - wb);
-  const int g0 = rank * n_loc;  // this CTA's first global position
-  const int t = threadIdx.x;
-  uint64_t r[4];
+  const int g0 = rank * kSortLoc;  // this CTA's first input position
+  const int n_here = max(0, min(kSortLoc, W - g0));
+  SL_SSTAMP();
+  RadixItems<2> it;
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int p = g0 + 4 * t + x;
-    r[x] = ~0ull ^ kPosMask ^ (uint64_t)(p & kPosMask);  // padding: top bit set, unique
-    if (p < W) {
-      const double d = fadd_(st.w_arrival[wb + p], st.w_ttft[wb + p]);  // > 0 (core.py:40-47)
-      r[x] = ((uint64_t)__double_as_longlong(d) & ~kPosMask) | (uint64_t)p;
+  for (int x = 0; x < 2; ++x) {
+    const int p = item_pos<2>(x);
+    it.ok[x] = p < n_here;
+    it.v[x] = it.ok[x] ? packed_key(st, wb, g0 + p) : 0ull;
+    if (it.ok[x]) sm.buf[0][p] = it.v[x];  // read by the tie check if no pass moves them
+  }
+  uint64_t gmin, gmax;
+  cluster_minmax<2>(sm, it.v, it.ok, gmin, gmax);
+  // the highest bit in which two keys differ is the highest bit of max ^ min
+  const uint64_t all = (gmin ^ gmax) >> kPosBits;
+  SL_SSTAMP();
+  bool tie = W > 1 && all == 0;  // every deadline shares its top 49 bits
+  bool done = tie;
+  if (!done && cs > 1) {
+    const int hb = kPosBits + 63 - __clzll((long long)all);  // top varying bit
+    done = msd_sort(sm, it, W, hb, gmin, gmax, wb, perm, &tie);
+  }
+  if (!done) {  // one CTA, or a skewed bucket distribution: cluster LSD passes
+    int cur = 0;
+    const int nbits = all ? 64 - __clzll((long long)all) : 0;
+    for (int b = 0; b < nbits; b += 8) cluster_pass(sm, it, cur, kPosBits + b, ImgKey{}, n_here);
+    bool t = false;
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int p = item_pos<2>(x);
+      if (!it.ok[x] || g0 + p + 1 >= W) continue;
+      const uint64_t nx = p + 1 < kSortLoc ? sm.buf[cur][p + 1]
+                                           : cl.map_shared_rank(sm.buf[cur], rank + 1)[0];
+      t |= near_tie(it.v[x], nx);
+    }
+    t = __syncthreads_or(t) != 0;
+    tie = cluster_or(sm, t) != 0;
+    cluster_bar();  // vall read before it is reused
+    if (!tie) {
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+        if (it.ok[x])
+          perm[wb + g0 + item_pos<2>(x)] = (int32_t)(wb + (int64_t)(it.v[x] & kPosMask));
     }
   }
-  bool in_smem = false;
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int j = size >> 1; j > 0; j >>= 1) {
-      if (j >= 128) {
-        if (!in_smem) {
+  if (tie && W > 0) {
+    // exact: positions sorted by id, then arrival, then deadline (stable passes)
+    int cur = 0;
 #pragma unroll
-          for (int x = 0; x < 4; ++x) key[4 * t + x] = r[x];
-          in_smem = true;
-        }
-        if (j >= n_loc) {
-          cl.sync();
-          const int pr = rank ^ (j / n_loc);
-          if (rank < pr) {
-            uint64_t* rk = cl.map_shared_rank(key, pr);
-            for (int i = t; i < n_loc; i += blockDim.x) {
-              const bool up = ((g0 + i) & size) == 0;
-              const uint64_t a = key[i], b = rk[i];
-              const bool ab = ldf_before(st, wb, a, b);
-              if (ab != up) {
-                key[i] = b;
-                rk[i] = a;
-              }
-            }
-          }
-          cl.sync();
-        } else {
-          __syncthreads();
-          for (int q = t; q < n_loc / 2; q += blockDim.x) {
-            const int lo = ((q & ~(j - 1)) << 1) | (q & (j - 1));
-            const bool up = ((g0 + lo) & size) == 0;
-            const uint64_t a = key[lo], b = key[lo + j];
-            const bool ab = ldf_before(st, wb, a, b);
-            if (ab != up) {
-              key[lo] = b;
-              key[lo + j] = a;
-            }
-          }
-          __syncthreads();
-        }
-        continue;
-      }
-      if (in_smem) {
+    for (int x = 0; x < 2; ++x) it.v[x] = (uint64_t)(g0 + item_pos<2>(x));
+    const int64_t* id = st.w_id + wb;
+    const double* arr = st.w_arrival + wb;
+    const double* tt = st.w_ttft + wb;
+    cluster_sort_on(sm, it, cur, 0, ImgId{id}(0), ImgId{id}, n_here);
+    cluster_sort_on(sm, it, cur, 0, ImgArr{arr}(0), ImgArr{arr}, n_here);
+    cluster_sort_on(sm, it, cur, 0, ImgDl{arr, tt}(0), ImgDl{arr, tt}, n_here);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) r[x] = key[4 * t + x];
-        in_smem = false;
-      }
-      if (j >= 4) {
-        const int tl = j >> 2;
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const int p = 4 * t + x;
-          const uint64_t o = __shfl_xor_sync(SL_FULL, r[x], tl);
-          const bool up = ((g0 + p) & size) == 0, lower = (p & j) == 0;
-          r[x] = ldf_first(st, wb, r[x], o, lower == up);
-        }
-      } else {  // j = 2: (0,2), (1,3); j = 1: (0,1), (2,3) -- static register indices
-        auto ce = [&](uint64_t& a, uint64_t& b, int x) {
-          const bool up = ((g0 + 4 * t + x) & size) == 0;
-          const bool ab = ldf_before(st, wb, a, b);
-          const uint64_t lo = ab == up ? a : b, hi = ab == up ? b : a;
-          a = lo;
-          b = hi;
-        };
-        if (j == 2) {
-          ce(r[0], r[2], 0);
-          ce(r[1], r[3], 1);
-        } else {
-          ce(r[0], r[1], 0);
-          ce(r[2], r[3], 2);
-        }
-      }
-    }
+    for (int x = 0; x < 2; ++x)
+      if (it.ok[x]) perm[wb + g0 + item_pos<2>(x)] = (int32_t)(wb + (int64_t)it.v[x]);
   }
-  if (in_smem) {
-    __syncthreads();
-#pragma unroll
-    for (int x = 0; x < 4; ++x) r[x] = key[4 * t + x];
-  }
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int p = g0 + 4 * t + x;
-    if (p < W) perm[wb + p] = (int32_t)(wb + (int64_t)(r[x] & kPosMask));
-  }
+  SL_SSTAMP();
 }
 
 }  // namespace
