@@ -804,6 +804,9 @@ __device__ __forceinline__ void cluster_minmax(RadixSmem& sm, const uint64_t (&v
   if (mn != ~0ull) atomicMin(&sm.kmin, (unsigned long long)mn);
   if (mx != 0) atomicMax(&sm.kmax, (unsigned long long)mx);
   __syncthreads();
+  // every CTA of the cluster has started (the kernel's arrive) before the first
+  // store into another CTA's shared memory
+  if (cs > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if ((int)threadIdx.x < cs) {
     cl.map_shared_rank(sm.vmin, (int)threadIdx.x)[rank] = sm.kmin;
     cl.map_shared_rank(sm.vmax, (int)threadIdx.x)[rank] = sm.kmax;
@@ -1103,7 +1106,7 @@ __device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W
 #pragma unroll
   for (int x = 0; x < 2; ++x) {
     const double dk = __longlong_as_double((long long)(in.v[x] & ~kPosMask));
-    d[x] = min(255, (int)((dk - dlo) * sc));
+    d[x] = in.ok[x] ? min(255, (int)((dk - dlo) * sc)) : 0;
     if (in.ok[x]) slot[x] = atomicAdd(&sm.lh[d[x]], 1u);
   }
   __syncthreads();
@@ -1195,8 +1198,8 @@ __device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W
   for (int x = 0; x < 4; ++x) {
     const double dk = __longlong_as_double((long long)(it.v[x] & ~kPosMask));
     const double xs = (dk - dlo) * sc;  // the MSD step's value: same bucket
-    const int B = min(255, (int)xs);
-    const int sub = min(K - 1, (int)((xs - (double)B) * (double)K));
+    const int B = it.ok[x] ? min(255, (int)xs) : 0;
+    const int sub = it.ok[x] ? min(K - 1, (int)((xs - (double)B) * (double)K)) : 0;
     ld[x] = sm.bidx[B] * K + sub;
     if (it.ok[x]) ls[x] = atomicAdd(&sm.lh[ld[x]], 1u);
   }
@@ -1311,6 +1314,9 @@ __global__ void __launch_bounds__(kSortCtaThreads) sort_cluster_kernel(const sl_
   const int g0 = rank * kSortLoc;  // this CTA's first input position
   const int n_here = max(0, min(kSortLoc, W - g0));
   SL_SSTAMP();
+  // arrive now, wait before the first DSMEM access (cluster_minmax): the key
+  // loads overlap the cluster's start-up
+  if (cs > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   RadixItems<2> it;
 #pragma unroll
   for (int x = 0; x < 2; ++x) {

@@ -12,12 +12,20 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _arrays(ws, seed, ties):
+def _arrays(ws, seed, ties, cluster=None):
     rng = np.random.default_rng(seed)
     W = int(sum(ws))
     S = len(ws)
     arr = 10.0 - rng.uniform(0.0, 0.4, W)
     ttft = np.array([0.5, 2.0, 7.5])[rng.integers(0, 3, W)]
+    if cluster:
+        # `cluster` keys of each segment with distinct deadlines 1e-8 s apart (far
+        # above the packed keys' 2^-34 s resolution: no near-ties), in random order
+        for b, e in zip(np.cumsum([0] + ws[:-1]), np.cumsum(ws)):
+            k = min(cluster, e - b)
+            sel = b + rng.permutation(e - b)[:k]
+            arr[sel] = 10.0 - 1e-8 * rng.permutation(k)
+            ttft[sel] = 2.0
     if ties:
         # arrivals on a coarse grid -> many equal deadlines (ties on arrival too),
         # plus near-ties: deadlines one ulp apart
@@ -45,6 +53,28 @@ CASES = {
     "cluster_8cta": [32768, 20000, 16385],
     "tiles": [3000] * 70,  # more than 64 segments: tile sort + merge passes
 }
+
+
+# clustered deadlines: 1,000 keys in one MSD bucket (the local sub-bucket pass
+# overflows -> LSD passes in that CTA), and almost every key in one bucket (the
+# distribution overflows a CTA -> cluster-wide LSD passes)
+CLUSTERED = {"dense_cluster": ([32768], 1000), "one_bucket": ([20000, 9000], 19990)}
+
+
+@pytest.mark.parametrize("case", list(CLUSTERED))
+def test_ldf_sort_clustered_deadlines(case):
+    from paper_2505_23022_b200.plan import PlanBatch
+
+    ws, k = CLUSTERED[case]
+    a = _arrays(ws, seed=5, ties=False, cluster=k)
+    pb = PlanBatch(arrays=a)
+    pb.sort()
+    perm = pb.o["perm"].cpu().numpy()
+    dl = a["w_arrival"] + a["w_ttft"]
+    for s in range(len(ws)):
+        b, e = int(a["w_begin"][s]), int(a["w_begin"][s + 1])
+        want = b + np.lexsort((a["w_id"][b:e], a["w_arrival"][b:e], dl[b:e]))
+        assert np.array_equal(perm[b:e], want), (case, s)
 
 
 @pytest.mark.parametrize("ties", [False, True], ids=["random", "ties"])
