@@ -763,6 +763,19 @@ constexpr int kSelCtaMaxSegments = 64;
 // that passes at the current prefix"), sum(1/slo), admission rounds, vbs, and
 // the credit phase.  Same decisions and fp64 values as seg_sort_warp +
 // seg_guard_admit + seg_credit_select (sched_scorpio.py:117-207, 210-316).
+#ifdef SL_LARGE_PROF
+__device__ unsigned long long sl_fused_prof[16];
+#define SL_FSTAMP()                                                 \
+  do {                                                              \
+    if (seg == 0 && lane == 0) {                                    \
+      const unsigned long long k_ = sl_fused_prof[0] + 1;           \
+      if (k_ < 16) sl_fused_prof[k_] = clock64();                   \
+      sl_fused_prof[0] = k_;                                        \
+    }                                                               \
+  } while (0)
+#else
+#define SL_FSTAMP() do {} while (0)
+#endif
 __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl_plan_config& cfg,
                                                const sl_plan_out& out, int seg, int lane,
                                                double* buf) {
@@ -779,6 +792,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
   const double now = st.now[seg];
   const int E = st.credit_exp[seg];
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  SL_FSTAMP();
   // ---- every input at once
   const bool wv = lane < W, rv = lane < R;
   double arr = 0.0, tt0 = 0.0, pf0 = 0.0, tp0 = 1.0;
@@ -803,6 +817,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
     rcred = st.r_credit[rb + lane];
     rex = st.r_exclude && st.r_exclude[rb + lane];
   }
+  SL_FSTAMP();
   // ---- LDF order (sched_scorpio.py:193): src = input position at walk position lane
   int src = lane;
   if (ttft_guard) {
@@ -855,6 +870,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
     }
     if (wv) out.perm[wb + lane] = (int32_t)(wb + src);
   }
+  SL_FSTAMP();
   // fields in walk order
   const double e = __shfl_sync(SL_FULL, fsub_(now, arr), src);
   const double pf = __shfl_sync(SL_FULL, pf0, src);
@@ -897,6 +913,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
       }
     }
   }
+  SL_FSTAMP();
   const unsigned rejw = vmask & ~kept;
   if ((rejw >> lane) & 1u) {
     out.w_status[idx] = SL_PLAN_REJECTED_TTFT;
@@ -931,6 +948,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
       ps_add_warp_smem(ps, frcp_(rt), R, buf);
       inv = ps_result(ps);
     }
+  SL_FSTAMP();
     // ---- admission rounds (:237-294): every pending candidate against one state
     const double ic = frcp_(tp);
     const bool solo = solo_ok(C, tp, ic, ln, pred);
@@ -974,6 +992,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
     min_d = fmin(min_d, v);
     has_min = has_min || kept != 0;
   }
+  SL_FSTAMP();
   const int nadm = __popc(admm);
   if ((admm >> lane) & 1u) {
     const int q = __popc(admm & lanemask_lt());
@@ -1001,10 +1020,11 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
       __syncwarp();
       if (a) buf[__popc(admm & lanemask_lt())] = x;
       __syncwarp();
-      for (int t = 0; t < nadm; ++t) ps_add(vs, buf[t]);
+      ps_fold_buf(vs, buf, nadm);
     }
     vbs = ps_result(vs);
   }
+  SL_FSTAMP();
   const uint64_t MIN = has_min ? slo_fixed<false>(min_d, E) : ~0ull;
   if (lane == 0) {
     out.seg_counts[4 * seg + 0] = __popc(keepm);
@@ -1034,6 +1054,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
     out.r_pos[rb + lane] = b ? __popc(bm & lanemask_lt()) : -1;
   }
   if (lane == 0) out.seg_counts[4 * seg + 3] = __popc(bm);
+  SL_FSTAMP();
 }
 
 // ---- the whole plan_step in one launch (segments of <= 32 waiting items):
@@ -1108,6 +1129,14 @@ int plan_cta_max() {
 }  // namespace
 
 #include "plan_large.cuh"
+
+#ifdef SL_LARGE_PROF
+extern "C" int sl_fused_prof_read(unsigned long long* out) {  // and reset
+  static const unsigned long long z[16] = {0};
+  if (cudaMemcpyFromSymbol(out, sl_fused_prof, sizeof(z)) != cudaSuccess) return SL_ERR_CUDA;
+  return cudaMemcpyToSymbol(sl_fused_prof, z, sizeof(z)) == cudaSuccess ? 0 : SL_ERR_CUDA;
+}
+#endif
 
 extern "C" {
 

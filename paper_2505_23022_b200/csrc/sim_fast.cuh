@@ -25,6 +25,9 @@ constexpr int kRunCap = 32 * kSlots;
 #ifndef SL_INV_UNROLL
 #define SL_INV_UNROLL 0  // unrolled branch-free 1/slo fold (measured: 112 -> 118 ms, registers)
 #endif
+#ifndef SL_INV_FOLD
+#define SL_INV_FOLD 0  // branch-free ps_add_nz loop for the 1/slo fold rebuild
+#endif
 #ifndef SL_WALK_SKIP
 #define SL_WALK_SKIP 1  // general steps skip the walk while now < walk_until
 #endif
@@ -123,6 +126,8 @@ __device__ __forceinline__ PySum running_inv_sum(const Sim& s, const Slot<WIDE> 
       }
 #pragma unroll
       for (int t = 0; t < 32; ++t) ps_add_nz(ps, v[t]);
+    } else if (SL_INV_FOLD) {
+      ps_fold_buf(ps, bc, cnt);
     } else {
       for (int t = 0; t < cnt; ++t) ps_add(ps, bc[t]);
     }

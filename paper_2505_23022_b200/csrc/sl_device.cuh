@@ -110,6 +110,18 @@ __device__ __forceinline__ void ps_add_warp_long(PySum& s, double x, int cnt) {
   }
 }
 
+// Fold buf[0, cnt) into s in order: the first term of an empty sum takes the
+// int-0 path, every later one the branch-free ps_add_nz (same result as ps_add).
+__device__ __forceinline__ void ps_fold_buf(PySum& s, const double* buf, int cnt) {
+  int t = 0;
+  if (s.n == 0 && cnt > 0) {
+    s.f = fadd_(0.0, buf[0]);
+    s.n = 1;
+    t = 1;
+  }
+  for (; t < cnt; ++t) ps_add_nz(s, buf[t]);
+}
+
 // As ps_add_warp_long with the operands gathered through a per-warp shared
 // buffer `buf` (32 doubles, 16-byte aligned) as 16 x LDS.128 broadcasts instead
 // of 64 shuffles: the fold is then bound by its own fp64 issue (~19 cycles per
@@ -119,7 +131,7 @@ __device__ __forceinline__ void ps_add_warp_smem(PySum& s, double x, int cnt, do
   __syncwarp();
   buf[lane] = x;
   __syncwarp();
-  if (cnt == 32 && s.n > 0) {
+  if (cnt == 32) {
     double v[32];
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
@@ -127,10 +139,17 @@ __device__ __forceinline__ void ps_add_warp_smem(PySum& s, double x, int cnt, do
       v[2 * t] = p.x;
       v[2 * t + 1] = p.y;
     }
+    if (s.n == 0) {  // first term of an empty sum: the int-0 path
+      s.f = fadd_(0.0, v[0]);
+      s.n = 1;
 #pragma unroll
-    for (int t = 0; t < 32; ++t) ps_add_nz(s, v[t]);
+      for (int t = 1; t < 32; ++t) ps_add_nz(s, v[t]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) ps_add_nz(s, v[t]);
+    }
   } else {
-    for (int t = 0; t < cnt; ++t) ps_add(s, buf[t]);
+    ps_fold_buf(s, buf, cnt);
   }
 }
 
