@@ -25,6 +25,9 @@ constexpr int kRunCap = 32 * kSlots;
 #ifndef SL_INV_UNROLL
 #define SL_INV_UNROLL 0  // unrolled branch-free 1/slo fold (measured: 112 -> 118 ms, registers)
 #endif
+#ifndef SL_QUIET_PIPE
+#define SL_QUIET_PIPE 0  // quiet loop: step k+1's batch formed during step k's clock update
+#endif
 #ifndef SL_INV_FOLD
 #define SL_INV_FOLD 0  // branch-free ps_add_nz loop for the 1/slo fold rebuild
 #endif
@@ -38,7 +41,7 @@ constexpr int kRunCap = 32 * kSlots;
 // sum of W over walks, sum of W over admission scans.
 #ifdef SL_PHASE_PROF
 constexpr int kProfSims = 1 << 16;
-constexpr int kProfSlots = 22;
+constexpr int kProfSlots = 26;
 __device__ __forceinline__ unsigned long long prof_gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -624,6 +627,50 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   uint32_t d_nb = 0, d_bh = 0;
   bool have = false;
   bool ret = false;
+#if SL_QUIET_PIPE
+  // One-step software pipeline: the credit recurrence does not depend on the
+  // clock, so step k+1's batch (credits, ballot, length / hash sums) is formed
+  // while step k's itl() chain is in flight, and committed only when step k+1
+  // runs (a retirement at step k, or the loop bound, discards it).
+  if (R > 0 && R <= 32 && now < lim) {
+    cred_t<WIDE> N1 = sl[0].N + g.Smin;
+    bool b1 = live && (all || N1 >= sl[0].S);
+    unsigned nb1 = __popc(__ballot_sync(SL_FULL, b1));
+    unsigned blen1 = __reduce_add_sync(SL_FULL, b1 ? (unsigned)sl[0].cur_len : 0u);
+    unsigned bh1 = __reduce_add_sync(SL_FULL, b1 ? hh : 0u);
+    for (;;) {
+      if (live && !all) sl[0].N = b1 ? N1 - sl[0].S : N1;
+      if (b1) {
+        sl[0].cur_len += 1;
+        sl[0].rem -= 1;
+      }
+      const int nb = (int)nb1;
+      const unsigned blen = blen1, bh = bh1;
+      ret = __any_sync(SL_FULL, live && sl[0].rem <= 0);
+      N1 = sl[0].N + g.Smin;  // step k+1, speculative
+      b1 = live && (all || N1 >= sl[0].S);
+      nb1 = __popc(__ballot_sync(SL_FULL, b1));
+      blen1 = __reduce_add_sync(SL_FULL, b1 ? (unsigned)sl[0].cur_len : 0u);
+      bh1 = __reduce_add_sync(SL_FULL, b1 ? hh : 0u);
+      const double end = fadd_(now, itl(C, nb, div_small((double)blen, nb)));
+      if (lane == (k & 31)) {
+        end_bits = (uint64_t)__double_as_longlong(end);
+        d_nb = nb;
+        d_bh = bh;
+        have = true;
+      }
+      now = end;
+      ++k;
+      if (ret || !(now < lim)) break;
+      if ((k & 31) == 0) {
+        if (have)
+          acc.dig += digest_item((uint64_t)(step0 + k - 32 + lane), 2, d_nb, d_bh) +
+                     digest_item((uint64_t)(step0 + k - 32 + lane), 3, 0, end_bits);
+        have = false;
+      }
+    }
+  }
+#else
   while (R > 0 && R <= 32 && now < lim) {
     const cred_t<WIDE> N = sl[0].N + g.Smin;
     const bool b = live && (all || N >= sl[0].S);  // all: decode-all policies, no credits
@@ -653,6 +700,7 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
       have = false;
     }
   }
+#endif
   if (have)
     acc.dig += digest_item((uint64_t)(step0 + ((k - 1) & ~31) + lane), 2, d_nb, d_bh) +
                digest_item((uint64_t)(step0 + ((k - 1) & ~31) + lane), 3, 0, end_bits);
@@ -790,6 +838,12 @@ __device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, i
       SL_PROF_MARK(1)
     } else {
     SL_PROF_COUNT(8, 1)
+    // general-step kinds: quiet-eligible but for R > 32 (nothing waiting / blocked
+    // with the walk bound ahead), and R > 32 at all
+    SL_PROF_COUNT(22, R > 32 && W == 0)
+    SL_PROF_COUNT(23, R > 32 && W > 0 && blocked && now < walk_until)
+    SL_PROF_COUNT(24, R > 32)
+    SL_PROF_COUNT(25, W > 0 && !blocked)
 #ifdef SL_PHASE_PROF
     prof_acc[12] = prof_acc[12] > (unsigned long long)W ? prof_acc[12] : (unsigned long long)W;
     prof_acc[13] = prof_acc[13] > (unsigned long long)R ? prof_acc[13] : (unsigned long long)R;

@@ -22,8 +22,10 @@ torch.cuda.synchronize()
 res = eng.results()
 lib = N.lib()
 lib.sl_phase_prof_read.argtypes = [C.c_void_p, C.c_int32]
-out = np.zeros((eng.n_sims, 22), np.uint64)
+out = np.zeros((eng.n_sims, 26), np.uint64)
 assert lib.sl_phase_prof_read(out.ctypes.data, eng.n_sims) == eng.n_sims
+k4 = out[:, 22:26].sum(axis=0)
+print('general steps: R>32 & W==0 %d, R>32 & blocked & walk ahead %d, R>32 %d, W>0 & not blocked %d' % tuple(int(x) for x in k4))
 names = ["arrivals+top", "quiet", "walk", "inv_sum", "admit", "decode", "tail", "retire",
          "gen_steps", "quiet_blocks", "quiet_steps", "gen_blocked", "maxW", "maxR"]
 cyc = out[:, :8].astype(np.float64)
