@@ -743,12 +743,13 @@ extern "C" int sl_large_prof_read(unsigned long long* out) {
 //     range of final positions (<= 4,096 keys; one more barrier).
 //  2. Each CTA LSD-sorts its range in shared memory (CTA barriers only).
 //  3. Adjacent sorted keys with equal top 49 bits (equal or near-equal
-//     deadlines; checked across CTA boundaries too) send the whole segment to
-//     the exact path: positions radix-sorted from input order by id, then
-//     arrival, then deadline (order-preserving 64-bit images), i.e. by the full
-//     sort key (deadline, arrival, id) and then position -- the stable order of
-//     list.sort (sched_scorpio.py:193).  A bucket distribution that would
-//     overflow a CTA falls back to cluster-wide LSD passes on the packed keys.
+//     deadlines) -- always inside one CTA's range, as equal deadline bits give
+//     equal buckets -- make that CTA re-sort its range by id, then arrival,
+//     then deadline (order-preserving 64-bit images, stable passes), i.e. by the
+//     full sort key (deadline, arrival, id) and then position -- the stable
+//     order of list.sort (sched_scorpio.py:193).  A bucket distribution that
+//     would overflow a CTA falls back to cluster-wide LSD passes on the packed
+//     keys, with a cluster-wide tie check and exact passes.
 //  Exact for every input.
 namespace {
 
@@ -773,9 +774,10 @@ struct RadixSmem {
   int32_t start[kSortMaxCluster + 1];  // MSD: first final position owned by each CTA
   uint32_t wsum[kSortWarps];
   unsigned long long vall[kSortMaxCluster];  // every CTA's flag word (pushed)
-  unsigned long long tfirst[kSortMaxCluster], tlast[kSortMaxCluster];  // MSD tie check
   unsigned long long vmin[kSortMaxCluster], vmax[kSortMaxCluster];    // key range exchange
   uint32_t lh[kLocalBins];             // bucket counts, then offsets (MSD: 256, local: 2048)
+  unsigned long long bmin[256], bmax[256];  // local: each owned bucket's key range
+  double bscale[256];
   unsigned long long vary, kmin, kmax;
 };
 
@@ -804,9 +806,6 @@ __device__ __forceinline__ void cluster_minmax(RadixSmem& sm, const uint64_t (&v
   if (mn != ~0ull) atomicMin(&sm.kmin, (unsigned long long)mn);
   if (mx != 0) atomicMax(&sm.kmax, (unsigned long long)mx);
   __syncthreads();
-  // every CTA of the cluster has started (the kernel's arrive) before the first
-  // store into another CTA's shared memory
-  if (cs > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if ((int)threadIdx.x < cs) {
     cl.map_shared_rank(sm.vmin, (int)threadIdx.x)[rank] = sm.kmin;
     cl.map_shared_rank(sm.vmax, (int)threadIdx.x)[rank] = sm.kmax;
@@ -1018,6 +1017,70 @@ __device__ __forceinline__ void local_pass(RadixSmem& sm, RadixItems<NS>& it, in
     if (it.ok[x]) it.v[x] = sm.buf[cur][item_pos<NS>(x)];
 }
 
+// One stable LSD pass inside the CTA on digit (IMG(item) >> shift) & 255.
+template <int NS, class Img>
+__device__ __forceinline__ void local_pass_img(RadixSmem& sm, RadixItems<NS>& it, int& cur,
+                                               int shift, const Img& img) {
+  const int w = threadIdx.x >> 5;
+  int d[NS];
+  uint32_t r[NS];
+#pragma unroll
+  for (int x = 0; x < NS; ++x) d[x] = it.ok[x] ? (int)((img(it.v[x]) >> shift) & 255u) : 0;
+  rank_digits<NS>(sm, d, it.ok, r);
+  uint64_t* dst = sm.buf[cur ^ 1];
+#pragma unroll
+  for (int x = 0; x < NS; ++x)
+    if (it.ok[x]) dst[sm.cnt[cidx(d[x], w)] + r[x]] = it.v[x];
+  __syncthreads();
+  cur ^= 1;
+#pragma unroll
+  for (int x = 0; x < NS; ++x)
+    if (it.ok[x]) it.v[x] = sm.buf[cur][item_pos<NS>(x)];
+}
+
+// CTA-local LSD sort of the items on the bits of IMG in which some item differs
+// from the first one (CTA barriers only).
+template <int NS, class Img>
+__device__ __forceinline__ void local_sort_on(RadixSmem& sm, RadixItems<NS>& it, int& cur, int n,
+                                              const Img& img) {
+  if (threadIdx.x == 0) sm.vary = 0;
+  __syncthreads();
+  const uint64_t ref = n > 0 ? img(sm.buf[cur][0]) : 0ull;
+  uint64_t v = 0;
+#pragma unroll
+  for (int x = 0; x < NS; ++x)
+    if (it.ok[x]) v |= img(it.v[x]) ^ ref;
+  const unsigned hi = __reduce_or_sync(SL_FULL, (unsigned)(v >> 32));
+  const unsigned lo = __reduce_or_sync(SL_FULL, (unsigned)v);
+  if ((threadIdx.x & 31) == 0 && (hi | lo))
+    atomicOr(&sm.vary, ((unsigned long long)hi << 32) | lo);
+  __syncthreads();
+  const uint64_t all = sm.vary;
+  const int nbits = all ? 64 - __clzll((long long)all) : 0;
+  for (int b = 0; b < nbits; b += 8) local_pass_img<NS>(sm, it, cur, b, img);
+}
+
+// Images of a packed key's position p (low 15 bits) for the exact order.
+struct KeyId {
+  const int64_t* id;
+  __device__ __forceinline__ uint64_t operator()(uint64_t k) const {
+    return (uint64_t)id[k & kPosMask] ^ (1ull << 63);
+  }
+};
+struct KeyArr {
+  const double* arr;
+  __device__ __forceinline__ uint64_t operator()(uint64_t k) const {
+    return dbl_ord(arr[k & kPosMask]);
+  }
+};
+struct KeyDl {
+  const double* arr;
+  const double* ttft;
+  __device__ __forceinline__ uint64_t operator()(uint64_t k) const {
+    return dbl_ord(fadd_(arr[k & kPosMask], ttft[k & kPosMask]));  // core.py:50-53
+  }
+};
+
 // Varying bits of IMG over the cluster's items, relative to `ref` (cluster barrier).
 template <class Img>
 __device__ __forceinline__ uint64_t cluster_vary(RadixSmem& sm, const RadixItems<2>& it,
@@ -1087,18 +1150,19 @@ __device__ __forceinline__ bool near_tie(uint64_t x, uint64_t nx) {
 // keys.  Otherwise writes the sorted positions to perm unless *tie (near-ties:
 // the caller runs the exact path).  Neither step needs to be stable: keys are
 // unique, and every key's final place is decided by the local sort.
-__device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W, int hb,
-                                         uint64_t gmin, uint64_t gmax, int64_t wb,
-                                         int32_t* perm, bool* tie) {
+__device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W, double dlo,
+                                         double dhi, int64_t wb,
+                                         const int64_t* sm_seg_id, const double* sm_seg_arr,
+                                         const double* sm_seg_tt, int32_t* perm, bool* tie) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int cs = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
-  // 1. bucket = floor(256 (d - dmin) / (dmax - dmin)), clamped: monotone in the
-  // key's deadline d (IEEE subtraction of, and multiplication by, a constant are
-  // monotone); slot inside the CTA's part of the bucket from a shared atomic
-  const double dlo = __longlong_as_double((long long)(gmin & ~kPosMask));
-  const double sc = 256.0 / (__longlong_as_double((long long)(gmax & ~kPosMask)) - dlo);
+  // 1. bucket = floor(256 (d - dlo) / (dhi - dlo)), clamped to [0, 255]: monotone
+  // in the key's deadline d (IEEE subtraction of, and multiplication by, a
+  // constant are monotone); slot inside the CTA's part of the bucket from a
+  // shared atomic
+  const double sc = 256.0 / (dhi - dlo);  // dhi > dlo
   if (threadIdx.x < 256) sm.lh[threadIdx.x] = 0;
   __syncthreads();
   int d[2];
@@ -1106,7 +1170,7 @@ __device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W
 #pragma unroll
   for (int x = 0; x < 2; ++x) {
     const double dk = __longlong_as_double((long long)(in.v[x] & ~kPosMask));
-    d[x] = in.ok[x] ? min(255, (int)((dk - dlo) * sc)) : 0;
+    d[x] = in.ok[x] ? min(255, max(0, (int)((dk - dlo) * sc))) : 0;
     if (in.ok[x]) slot[x] = atomicAdd(&sm.lh[d[x]], 1u);
   }
   __syncthreads();
@@ -1190,17 +1254,42 @@ __device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W
     it.v[x] = it.ok[x] ? sm.buf[0][item_pos<4>(x)] : 0ull;
   }
   for (int i = threadIdx.x; i < kLocalBins; i += blockDim.x) sm.lh[i] = 0;
+  if (threadIdx.x < 256) {
+    sm.bmin[threadIdx.x] = ~0ull;
+    sm.bmax[threadIdx.x] = 0;
+  }
   __syncthreads();
   const int K = kLocalBins / max(1, sm.nmine);
+  // each owned bucket's own key range (deadline bits: positive doubles order
+  // like their bits), so clamped edge buckets and gaps cost nothing
+  int B[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint64_t kb = it.v[x] & ~kPosMask;
+    const double xs = (__longlong_as_double((long long)kb) - dlo) * sc;  // the MSD bucket
+    B[x] = it.ok[x] ? min(255, max(0, (int)xs)) : 0;
+    if (it.ok[x]) {
+      atomicMin(&sm.bmin[B[x]], (unsigned long long)kb);
+      atomicMax(&sm.bmax[B[x]], (unsigned long long)kb);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 256 && sm.bmax[threadIdx.x] != 0) {
+    const double lo = __longlong_as_double((long long)sm.bmin[threadIdx.x]);
+    const double hi = __longlong_as_double((long long)sm.bmax[threadIdx.x]);
+    sm.bscale[threadIdx.x] = hi > lo ? (double)K / (hi - lo) : 0.0;
+  }
+  __syncthreads();
   int ld[4];
   uint32_t ls[4];
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
-    const double dk = __longlong_as_double((long long)(it.v[x] & ~kPosMask));
-    const double xs = (dk - dlo) * sc;  // the MSD step's value: same bucket
-    const int B = it.ok[x] ? min(255, (int)xs) : 0;
-    const int sub = it.ok[x] ? min(K - 1, (int)((xs - (double)B) * (double)K)) : 0;
-    ld[x] = sm.bidx[B] * K + sub;
+    const uint64_t kb = it.v[x] & ~kPosMask;
+    const double lo = __longlong_as_double((long long)sm.bmin[B[x]]);
+    const int sub = it.ok[x] ? min(K - 1, max(0, (int)((__longlong_as_double((long long)kb) - lo) *
+                                                        sm.bscale[B[x]])))
+                             : 0;
+    ld[x] = sm.bidx[B[x]] * K + sub;
     if (it.ok[x]) ls[x] = atomicAdd(&sm.lh[ld[x]], 1u);
   }
   __syncthreads();
@@ -1264,39 +1353,27 @@ __device__ __forceinline__ bool msd_sort(RadixSmem& sm, RadixItems<2>& in, int W
   SL_SSTAMP();
   SL_CTASTAMP(1, sl_gtime());
   SL_CTASTAMP(2, big);
-  // 3. near-tie check inside the range, then across ranges (first / last keys pushed)
+  // 3. near-ties (equal top 49 bits) have equal bucket values, so they share an
+  // owner: check adjacent keys inside the range only, and on a near-tie re-sort
+  // the range with the full key -- id, then arrival, then deadline, stable
+  // CTA-local passes (the packed order, i.e. position, breaks exact ties).
+  // No cluster-wide decision: the CTAs finish independently.
   bool t = false;
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
     const int p = item_pos<4>(x);
     if (it.ok[x] && p + 1 < my_n) t |= near_tie(it.v[x], sm.buf[cur][p + 1]);
   }
-  t = __syncthreads_or(t) != 0;
-  if ((int)threadIdx.x < cs) {
-    const int q = (int)threadIdx.x;
-    const unsigned long long fl = my_n ? sm.buf[cur][0] : ~0ull;
-    const unsigned long long la = my_n ? sm.buf[cur][my_n - 1] : ~0ull;
-    cl.map_shared_rank(sm.tfirst, q)[rank] = fl;
-    cl.map_shared_rank(sm.tlast, q)[rank] = la;
+  if (__syncthreads_or(t)) {
+    const int64_t* idp = sm_seg_id;
+    local_sort_on<4>(sm, it, cur, my_n, KeyId{idp});
+    local_sort_on<4>(sm, it, cur, my_n, KeyArr{sm_seg_arr});
+    local_sort_on<4>(sm, it, cur, my_n, KeyDl{sm_seg_arr, sm_seg_tt});
   }
-  const bool any = cluster_or(sm, t) != 0;  // its barrier also publishes tfirst / tlast
-  bool bt = false;
-  {
-    unsigned long long prev = ~0ull;  // last key of the previous non-empty range
-    for (int c = 0; c < cs; ++c) {
-      if (sm.tfirst[c] == ~0ull) continue;
-      if (prev != ~0ull) bt |= near_tie(prev, sm.tfirst[c]);
-      prev = sm.tlast[c];
-    }
-  }
-  *tie = any || bt;  // the same in every CTA
-  if (!*tie) {
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
-      if (it.ok[x]) perm[wb + my_start + item_pos<4>(x)] = (int32_t)(wb + (int64_t)(it.v[x] & kPosMask));
-  } else {
-    cluster_bar();  // tfirst / vall read everywhere before the exact path reuses them
-  }
+  for (int x = 0; x < 4; ++x)
+    if (it.ok[x]) perm[wb + my_start + item_pos<4>(x)] = (int32_t)(wb + (int64_t)(it.v[x] & kPosMask));
+  *tie = false;
   return true;  // no DSMEM access is pending: CTAs may exit
 }
 
@@ -1325,18 +1402,40 @@ __global__ void __launch_bounds__(kSortCtaThreads) sort_cluster_kernel(const sl_
     it.v[x] = it.ok[x] ? packed_key(st, wb, g0 + p) : 0ull;
     if (it.ok[x]) sm.buf[0][p] = it.v[x];  // read by the tie check if no pass moves them
   }
-  uint64_t gmin, gmax;
-  cluster_minmax<2>(sm, it.v, it.ok, gmin, gmax);
-  // the highest bit in which two keys differ is the highest bit of max ^ min
-  const uint64_t all = (gmin ^ gmax) >> kPosBits;
-  SL_SSTAMP();
-  bool tie = W > 1 && all == 0;  // every deadline shares its top 49 bits
-  bool done = tie;
-  if (!done && cs > 1) {
-    const int hb = kPosBits + 63 - __clzll((long long)all);  // top varying bit
-    done = msd_sort(sm, it, W, hb, gmin, gmax, wb, perm, &tie);
+  // bucket range from a fixed sample of 128 keys, read by every CTA from global
+  // memory (no exchange needed: every CTA computes the same range)
+  if (threadIdx.x == 0) {
+    sm.kmin = ~0ull;
+    sm.kmax = 0;
   }
-  if (!done) {  // one CTA, or a skewed bucket distribution: cluster LSD passes
+  __syncthreads();
+  if ((int)threadIdx.x < min(W, 128)) {
+    const int p = W >= 128 ? (int)(((int64_t)threadIdx.x * W) >> 7) : (int)threadIdx.x;
+    const uint64_t k = packed_key(st, wb, p) & ~kPosMask;
+    atomicMin(&sm.kmin, (unsigned long long)k);
+    atomicMax(&sm.kmax, (unsigned long long)k);
+  }
+  __syncthreads();
+  const double slo = __longlong_as_double((long long)sm.kmin);
+  const double shi = __longlong_as_double((long long)sm.kmax);
+  // every CTA of the cluster has started (the arrive above) before the first
+  // store into another CTA's shared memory
+  if (cs > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  SL_SSTAMP();
+  bool tie = false;
+  bool done = false;
+  if (cs > 1 && W > 1 && slo < shi)
+    done = msd_sort(sm, it, W, slo, shi, wb, st.w_id + wb, st.w_arrival + wb, st.w_ttft + wb,
+                    perm, &tie);
+  uint64_t all = 0;  // bits 15.. in which two keys differ (the highest: that of max ^ min)
+  if (!done) {  // one CTA, a sample without spread, or a skewed bucket distribution:
+                // cluster LSD passes on the varying bits
+    uint64_t gmin, gmax;
+    cluster_minmax<2>(sm, it.v, it.ok, gmin, gmax);
+    all = (gmin ^ gmax) >> kPosBits;
+    tie = W > 1 && all == 0;  // every deadline shares its top 49 bits
+  }
+  if (!done && !tie) {
     int cur = 0;
     const int nbits = all ? 64 - __clzll((long long)all) : 0;
     for (int b = 0; b < nbits; b += 8) cluster_pass(sm, it, cur, kPosBits + b, ImgKey{}, n_here);
