@@ -17,9 +17,10 @@ request at plan_step entry processed by one scheduler iteration of one sim
 (SURVEY 8(d)); the device counts them exactly per sim.
 
 `e2e` is the same metric through the public API from host arrays: each step
-packs the cell table (pack_cells), uploads traces + cells (BatchEngine), runs
-the sweep and reads the result rows back (plus the NCCL gather when N > 1),
-wall-clock timed with the device synchronised on both sides.
+packs the cell table (pack_cells over the cells' columns), uploads the traces
+from a pinned host TraceTable and the cells (BatchEngine), runs the sweep and
+reads the result rows back (plus the NCCL gather when N > 1), wall-clock timed
+with the device synchronised on both sides.
 
 `--impl reference` times the UNMODIFIED reference (`slosim`, pure Python,
 installed in baseline/_ref by tools/install_reference.sh) through its own
@@ -643,7 +644,14 @@ def run_ours(args) -> None:
     # e2e: the public API from host arrays, every step: pack the cell table,
     # upload traces + cells (BatchEngine), sweep, read the result rows back
     # (+ gather when N > 1); wall clock with the device synchronised both sides
-    cells = build_cells(grid, owned, traces)
+    # inputs as a user holds them: the rank's traces in one pinned host table
+    # (TraceTable) and its cells as columns sharing the grid's config
+    from paper_2505_23022_b200.batch import CellColumns, TraceTable
+
+    table = TraceTable(traces)
+    cl = build_cells(grid, owned, traces)
+    cells = CellColumns(np.array([c.trace for c in cl], np.int64),
+                        np.array([c.slo_scale for c in cl]), grid.config)
     h2d = sum(getattr(t, k).nbytes for t in traces for k in
               ("arrival", "ttft_slo", "tpot_slo", "prompt_len", "true_out", "predicted", "id"))
     h2d += 8 * (len(traces) + 1) + len(cells) * (N.SIM_DTYPE.itemsize + 4)  # + begin, order
@@ -655,7 +663,7 @@ def run_ours(args) -> None:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        e = BatchEngine(traces, cells, device=dev)
+        e = BatchEngine(table, cells, device=dev)
         e.launch(stream)
         rows = e.results()  # D2H of the result rows (synchronises)
         if world > 1:
@@ -726,7 +734,7 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu,
             "e2e": {"value": total_rs / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e,
-                    "timed": "pack_cells + BatchEngine upload from host arrays + sweep + "
+                    "timed": "pack_cells (cell columns) + BatchEngine upload from the pinned host trace table + sweep + "
                              "result-row read-back (+ gather), wall clock"},
             "gpu_launches": args.steps * N.lib().sl_run_batch_launches(),
             "clocks": clk.summary(),

@@ -118,6 +118,75 @@ class Cell:
     rate_factor: float = 1.0
 
 
+@dataclass
+class CellColumns:
+    """Many cells sharing one config, as columns (the sweep's form): trace index,
+    SLO scale and rate factor per cell.  pack_cells handles it without a
+    per-cell Python loop."""
+    trace: np.ndarray
+    slo_scale: np.ndarray
+    config: CellConfig = field(default_factory=CellConfig)
+    rate_factor: np.ndarray | None = None
+
+    def __post_init__(self) -> None:
+        self.trace = np.ascontiguousarray(self.trace, np.int64)
+        self.slo_scale = np.ascontiguousarray(self.slo_scale, np.float64)
+        self.rate_factor = (np.ones(len(self.trace)) if self.rate_factor is None else
+                            np.ascontiguousarray(self.rate_factor, np.float64))
+        if not (len(self.slo_scale) == len(self.trace) == len(self.rate_factor)):
+            raise ValueError("cell columns must have equal length")
+
+    def __len__(self) -> int:
+        return len(self.trace)
+
+
+class _TraceMeta:
+    """Per-trace facts pack_cells / default_order need: lengths, last arrival,
+    distinct TPOT SLOs, longest prompt, longest prompt + output."""
+
+    def __init__(self, traces) -> None:
+        self.lens = np.array([len(t) for t in traces], np.int64)
+        self.last = np.array([float(t.arrival[-1]) if len(t) else 0.0 for t in traces])
+        self.uniq_tpot = [np.unique(t.tpot_slo) for t in traces]
+        self.max_prompt = np.array([int(t.prompt_len.max()) if len(t) else 0 for t in traces],
+                                   np.int64)
+        self.max_total = np.array(
+            [int((t.prompt_len.astype(np.int64) + t.true_out).max()) if len(t) else 0
+             for t in traces], np.int64)
+
+
+class TraceTable:
+    """Many traces as ONE host SoA (concatenated, `begin` offsets), in pinned
+    memory when CUDA is available -- the form BatchEngine uploads with async
+    copies -- plus the per-trace facts cell packing needs.  Build it once per
+    set of traces; every BatchEngine over it then copies from pinned memory."""
+
+    def __init__(self, traces: list[TraceArrays], pin: bool = True) -> None:
+        import torch
+
+        self.meta = _TraceMeta(traces)
+        self.n = len(traces)
+        self.begin = np.zeros(self.n + 1, np.int64)
+        np.cumsum(self.meta.lens, out=self.begin[1:])
+        self.categories = [t.category for t in traces]
+        pin = pin and torch.cuda.is_available()
+        self.host = {}
+        for k in TRACE_FIELDS:
+            a = (np.concatenate([getattr(t, k) for t in traces]) if traces else
+                 np.zeros(0, _TRACE_DTYPES[k]))
+            ht = torch.from_numpy(np.ascontiguousarray(a))
+            self.host[k] = ht.pin_memory() if pin else ht
+        bt = torch.from_numpy(self.begin.copy())
+        self.host["begin"] = bt.pin_memory() if pin else bt
+
+    def __len__(self) -> int:
+        return self.n
+
+
+def _meta(traces) -> _TraceMeta:
+    return traces.meta if isinstance(traces, TraceTable) else _TraceMeta(traces)
+
+
 _MIN_NORMAL = 2.2250738585072014e-308
 
 
@@ -156,51 +225,63 @@ def _config_row(cfg: CellConfig) -> tuple:
             float(cfg.horizon) if cfg.horizon is not None else 0.0, a, b, g, d, e, phi, th, ap, bp)
 
 
-def pack_cells(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = False,
+def pack_cells(traces, cells, outcomes: bool = False,
                log_cells: list[int] | None = None) -> np.ndarray:
     """Build the sl_sim table (host), column-wise: per-config rows are validated
     once per distinct config object, credit exponents per trace for all its
-    cells at once, workspace/outcome offsets by prefix sum."""
+    cells at once, workspace/outcome offsets by prefix sum.  `traces`: a list of
+    TraceArrays or a TraceTable; `cells`: a list of Cell or a CellColumns (one
+    config, no per-cell Python work)."""
     n = len(cells)
     sims = np.zeros(n, N.SIM_DTYPE)
     if n == 0:
         return sims
-    tr_idx = np.fromiter((c.trace for c in cells), np.int64, n)
-    scale = np.fromiter((c.slo_scale for c in cells), np.float64, n)
-    factor = np.fromiter((c.rate_factor for c in cells), np.float64, n)
+    meta = _meta(traces)
+    if isinstance(cells, CellColumns):
+        tr_idx, scale, factor = cells.trace, cells.slo_scale, cells.rate_factor
+        keys = np.zeros(n, np.int64)
+        table = [_config_row(cells.config)]
+    else:
+        tr_idx = np.fromiter((c.trace for c in cells), np.int64, n)
+        scale = np.fromiter((c.slo_scale for c in cells), np.float64, n)
+        factor = np.fromiter((c.rate_factor for c in cells), np.float64, n)
+        rows: dict[int, tuple] = {}
+        keys = np.empty(n, np.int64)
+        table = []
+        for k, c in enumerate(cells):
+            key = id(c.config)
+            r = rows.get(key)
+            if r is None:
+                r = rows[key] = (len(table), c.config)
+                table.append(_config_row(c.config))
+            keys[k] = r[0]
     if not ((scale > 0).all() and (factor > 0).all()):
         raise ValueError("slo_scale and rate_factor must be positive")
-    rows: dict[int, tuple] = {}
-    keys = np.empty(n, np.int64)
-    table = []
-    for k, c in enumerate(cells):
-        key = id(c.config)
-        r = rows.get(key)
-        if r is None:
-            r = rows[key] = (len(table), c.config)
-            table.append(_config_row(c.config))
-        keys[k] = r[0]
+    if ((tr_idx < 0) | (tr_idx >= len(meta.lens))).any():
+        raise ValueError("cell trace index out of range")
     cols = {name: np.array([row[j] for row in table])[keys]
             for j, name in enumerate(("policy", "flags", "max_batch_size", "horizon")
                                      + N.COST_FIELDS)}
-    lens = np.array([len(t) for t in traces], np.int64)
+    lens = meta.lens
     flags = cols["flags"].astype(np.int32)
     E = np.zeros(n, np.int32)
     wide = np.zeros(n, np.int32)
+    # credit exponents: one vectorised call per distinct set of TPOT SLOs (a sweep's
+    # traces share one SLO table), over every cell of the traces that have it
+    groups: dict[bytes, list[int]] = {}
     for t in np.unique(tr_idx):
-        sel = np.nonzero(tr_idx == t)[0]
-        tt = traces[int(t)]
-        E[sel], wide[sel] = credit_params_many(np.unique(tt.tpot_slo), scale[sel])
-        if len(tt):
-            big = int(tt.prompt_len.max())
-            # the fast kernel sums up to 64 current lengths in 32 bits
-            if int((tt.prompt_len.astype(np.int64) + tt.true_out).max()) >= 1 << 26:
-                flags[sel] |= N.FLAG_GENERAL_ONLY
-            # a negative prefill_time (alpha_p < 0 past -beta_p/alpha_p) breaks the
-            # fast kernel's monotone-prefix walk shortcuts: exact general kernel
-            ap, bp, th = cols["alpha_p"][sel], cols["beta_p"][sel], cols["theta"][sel]
-            neg = (ap < 0) & (big > th) & (ap * float(big) + bp < 0)
-            flags[sel[neg]] |= N.FLAG_GENERAL_ONLY
+        groups.setdefault(meta.uniq_tpot[int(t)].tobytes(), []).append(int(t))
+    for tlist in groups.values():
+        sel = np.nonzero(np.isin(tr_idx, tlist))[0]
+        E[sel], wide[sel] = credit_params_many(meta.uniq_tpot[tlist[0]], scale[sel])
+    nonempty = lens[tr_idx] > 0
+    # the fast kernel sums up to 64 current lengths in 32 bits
+    flags[nonempty & (meta.max_total[tr_idx] >= 1 << 26)] |= N.FLAG_GENERAL_ONLY
+    # a negative prefill_time (alpha_p < 0 past -beta_p/alpha_p) breaks the fast
+    # kernel's monotone-prefix walk shortcuts: exact general kernel
+    big = meta.max_prompt[tr_idx].astype(np.float64)
+    ap, bp, th = cols["alpha_p"], cols["beta_p"], cols["theta"]
+    flags[nonempty & (ap < 0) & (big > th) & (ap * big + bp < 0)] |= N.FLAG_GENERAL_ONLY
     ws = np.zeros(n, np.int64)
     np.cumsum(lens[tr_idx][:-1], out=ws[1:])
     log_slot = np.full(n, -1, np.int32)
@@ -226,7 +307,8 @@ def pack_cells(traces: list[TraceArrays], cells: list[Cell], outcomes: bool = Fa
 class BatchEngine:
     """Device buffers + launch for one batch of cells (reusable across launches)."""
 
-    def __init__(self, traces: list[TraceArrays], cells: list[Cell] | np.ndarray,
+    def __init__(self, traces: "list[TraceArrays] | TraceTable",
+                 cells: "list[Cell] | CellColumns | np.ndarray",
                  outcomes: bool = False, log_cells: list[int] | None = None,
                  log_steps: int = 0, log_ids: int = 0, order: np.ndarray | None = None,
                  device=None, mode: int = N.MODE_AUTO, log_skips: int = 0):
@@ -240,18 +322,23 @@ class BatchEngine:
         self.n_sims = len(sims)
         self.sims_host = sims
         self.mode = mode
-        lens = np.array([len(t) for t in traces], np.int64)
-        begin = np.zeros(len(traces) + 1, np.int64)
-        np.cumsum(lens, out=begin[1:])
-        self.trace_begin = begin
         dev = self.device
 
         def up(a):
             return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
-        self._tr = {k: up(np.concatenate([getattr(t, k) for t in traces]) if traces else
-                          np.zeros(0, _TRACE_DTYPES[k])) for k in TRACE_FIELDS}
-        self._tr["begin"] = up(begin)
+        if isinstance(traces, TraceTable):  # async copies from pinned host memory
+            lens = traces.meta.lens
+            self.trace_begin = traces.begin
+            self._tr = {k: v.to(dev, non_blocking=True) for k, v in traces.host.items()}
+        else:
+            lens = np.array([len(t) for t in traces], np.int64)
+            begin = np.zeros(len(traces) + 1, np.int64)
+            np.cumsum(lens, out=begin[1:])
+            self.trace_begin = begin
+            self._tr = {k: up(np.concatenate([getattr(t, k) for t in traces]) if traces else
+                              np.zeros(0, _TRACE_DTYPES[k])) for k in TRACE_FIELDS}
+            self._tr["begin"] = up(begin)
         if order is None:
             order = default_order(traces, sims)
         self._sims = up(sims.view(np.uint8))
@@ -436,8 +523,9 @@ def default_order(traces: list[TraceArrays], sims: np.ndarray) -> np.ndarray:
     longest step chains, so they start first."""
     if len(sims) == 0:
         return np.zeros(0, np.int32)
-    n_tr = np.array([len(t) for t in traces], np.float64)
-    last = np.array([float(t.arrival[-1]) if len(t) else 0.0 for t in traces])
+    meta = _meta(traces)
+    n_tr = meta.lens.astype(np.float64)
+    last = meta.last
     ti = sims["trace"].astype(np.int64)
     span = last[ti] / sims["rate_factor"]
     with np.errstate(divide="ignore", invalid="ignore"):
