@@ -393,6 +393,22 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
         out[name] = {"request_steps": Wt + Rt, "us_per_step": 1e6 * best,
                      "request_steps_per_s": (Wt + Rt) / best, "kernels": rows}
         del pb
+    # the harness floor: a one-element torch kernel timed the same way (behind the
+    # sleep, L2 flushed) -- what any single launch costs here before its own work
+    x = torch.zeros(1, device=dev)
+    floor = []
+    for it in range(reps + 2):
+        l2.zero_()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(200_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        x.add_(1.0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it >= 2:
+            floor.append(e0.elapsed_time(e1) * 1e3)
+    out["launch_floor_us"] = float(np.mean(floor))
     return out
 
 

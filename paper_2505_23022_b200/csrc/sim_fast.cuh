@@ -25,6 +25,17 @@ constexpr int kRunCap = 32 * kSlots;
 #ifndef SL_INV_UNROLL
 #define SL_INV_UNROLL 0  // unrolled branch-free 1/slo fold (measured: 112 -> 118 ms, registers)
 #endif
+#ifndef SL_ACC_SMEM
+#define SL_ACC_SMEM 0  // per-lane outcome counters in shared memory instead of registers
+#endif
+#if SL_ACC_SMEM
+constexpr int kAccWarps = 4;  // == kFastWarps (sim_kernel.cu)
+enum { kAccCompleted, kAccCompliant, kAccRejTtft, kAccRejAdm, kAccTtftViol, kAccTpotViol };
+__shared__ int32_t sl_acc_sm[kAccWarps][6][32];
+#define SL_ACC_ADD(acc, field, K, v) (sl_acc_sm[threadIdx.x >> 5][K][threadIdx.x & 31] += (v))
+#else
+#define SL_ACC_ADD(acc, field, K, v) ((acc).field += (v))
+#endif
 #ifndef SL_QUIET_PIPE
 #define SL_QUIET_PIPE 0  // quiet loop: step k+1's batch formed during step k's clock update
 #endif
@@ -297,7 +308,7 @@ __device__ __forceinline__ bool spec_walk(const Sim& s, const KArgs& a, bool has
       const int pos = nrej + __popc(rejm & lanemask_lt());
       const int64_t rid = s.id[idx];
       acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u);
-      acc.rej_ttft++;
+      SL_ACC_ADD(acc, rej_ttft, kAccRejTtft, 1);
       if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_TTFT;
       if (lg_rej >= 0 && pos < cap_rej) a.log.rej_ids[lg_rej + pos] = rid * 2;
     }
@@ -454,7 +465,7 @@ __device__ __forceinline__ bool spec_admit(const Sim& s, const KArgs& a, bool ha
       const int64_t rid = s.id[idx];  // ids only for decided requests
       int pos = nrej + __popc(rm & lanemask_lt());
       acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u + 1u);
-      acc.rej_adm++;
+      SL_ACC_ADD(acc, rej_adm, kAccRejAdm, 1);
       if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_ADMISSION;
       if (lg_rej >= 0 && pos < cap_rej) a.log.rej_ids[lg_rej + pos] = rid * 2 + 1;
     }
@@ -562,10 +573,10 @@ __device__ __forceinline__ void retire(const Sim& s, const KArgs& a, bool has_ou
       const double tpot = tout == 1 ? 0.0 : fdiv_(fsub_(end, first), (double)(tout - 1));
       const double ttft = fsub_(first, w.arr);
       const bool okc = ttft <= w.ttft && tpot <= w.tpot;
-      acc.completed++;
-      acc.compliant += okc;
-      acc.ttft_viol += ttft > w.ttft;
-      acc.tpot_viol += tpot > w.tpot;
+      SL_ACC_ADD(acc, completed, kAccCompleted, 1);
+      SL_ACC_ADD(acc, compliant, kAccCompliant, okc);
+      SL_ACC_ADD(acc, ttft_viol, kAccTtftViol, ttft > w.ttft);
+      SL_ACC_ADD(acc, tpot_viol, kAccTpotViol, tpot > w.tpot);
       if (has_out) {
         const int64_t o = s.out_off + idx;
         a.out.status[o] = SL_COMPLETED;
@@ -785,6 +796,10 @@ __device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, i
   bool log_over = false;
 
   Acc acc = {0, 0, 0, 0, 0, 0, 0, 0};
+#if SL_ACC_SMEM
+#pragma unroll
+  for (int k = 0; k < 6; ++k) sl_acc_sm[threadIdx.x >> 5][k][lane] = 0;
+#endif
   Slot<WIDE> sl[kSlots];
 #pragma unroll
   for (int k = 0; k < kSlots; ++k) {
@@ -1079,6 +1094,14 @@ __device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, i
   }
   SL_PROF_WRITE(si)
 
+#if SL_ACC_SMEM
+  acc.completed = sl_acc_sm[threadIdx.x >> 5][kAccCompleted][lane];
+  acc.compliant = sl_acc_sm[threadIdx.x >> 5][kAccCompliant][lane];
+  acc.rej_ttft = sl_acc_sm[threadIdx.x >> 5][kAccRejTtft][lane];
+  acc.rej_adm = sl_acc_sm[threadIdx.x >> 5][kAccRejAdm][lane];
+  acc.ttft_viol = sl_acc_sm[threadIdx.x >> 5][kAccTtftViol][lane];
+  acc.tpot_viol = sl_acc_sm[threadIdx.x >> 5][kAccTpotViol][lane];
+#endif
   write_result(a, si, acc, status | (log_over ? SL_SIM_LOG_OVERFLOW : 0), n, step, n_plans,
                n_idle, req_steps, now, has_h, s.horizon, lane);
 }

@@ -11,6 +11,9 @@ import bench  # noqa: E402
 peak, _ = bench.peaks()
 r = bench.plan_microbench(torch.device("cuda", 0), peak)
 for k, v in r.items():
+    if not isinstance(v, dict):
+        print(k, round(v, 2))
+        continue
     print(k, round(v["us_per_step"], 2), {kk: (round(vv["us"], 2), round(vv["frac"], 3))
                                             for kk, vv in v["kernels"].items()})
 if len(sys.argv) > 1:
