@@ -1209,8 +1209,23 @@ int sl_guard_admit_batch(const sl_plan_state* st, const sl_plan_config* cfg, sl_
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(guard_admit_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smem);
-    guard_admit_cta_kernel<<<st->n_segments, kLThreads, smem, (cudaStream_t)stream>>>(*st, *cfg,
-                                                                                      *out);
+    // a 2-CTA cluster per segment: the CPython folds on their own SM (SL_PLAN_SPLIT=0: one CTA)
+    const char* e = getenv("SL_PLAN_SPLIT");
+    const int cs = (e && e[0] == '0') ? 1 : 2;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(st->n_segments * cs);
+    lc.blockDim = dim3(kLThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, guard_admit_cta_kernel, *st, *cfg, *out) != cudaSuccess)
+      return SL_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
   }
   if (st->n_segments >= plan_group_min()) {

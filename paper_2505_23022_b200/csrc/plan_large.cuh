@@ -44,6 +44,7 @@ constexpr int kBarRed = 3;    // F1..F3 reduction
 constexpr int kBarVbs = 4;    // vbs pair (fold over running) -> warp 0
 constexpr int kBarInvRing = 5;   // 5..8: inv fold handover (full x2, empty x2)
 constexpr int kBarVbsRing = 9;   // 9..12: vbs fold handover
+constexpr int kBarInvPair = 13;  // split launch: the inv f / c warps
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -119,7 +120,21 @@ struct LargeSmem {
   long long lens;  // sum of current lengths over running
   double red_min[2];
   long long red_len[2];
+  int agg_ready, inv_ready, vbs_ready;  // split launch: set by the fold CTA, polled by warp 0
 };
+
+// Split launch (a cluster of 2 CTAs per segment): the fold warps run in CTA 1 on
+// their own SM and publish their results into CTA 0's shared memory, then set a
+// ready flag there (release at cluster scope); warp 0 of CTA 0 polls the flag
+// (acquire) where it would otherwise wait on the named barrier.
+__device__ __forceinline__ void flag_release(int* remote_flag) {
+  __threadfence();  // the results (DSMEM stores) before the flag
+  *reinterpret_cast<volatile int*>(remote_flag) = 1;
+}
+__device__ __forceinline__ void flag_acquire(const int* local_flag) {
+  while (*reinterpret_cast<const volatile int*>(local_flag) == 0) __nanosleep(64);
+  __threadfence();  // the flag before the results
+}
 
 // exclusive scan of the kLChunks counts of row r (warp 0), totals to *tot
 __device__ __forceinline__ void chunk_scan(LargeSmem& sm, int r, int lane, int* tot) {
@@ -295,8 +310,23 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
                                                                        sl_plan_out out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LargeSmem& sm = *reinterpret_cast<LargeSmem*>(smem_raw);
-  const int seg = blockIdx.x;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  // split: a 2-CTA cluster per segment -- CTA 0 walks and admits, CTA 1 folds
+  const bool split = cl.num_blocks() == 2;
+  const int crank = split ? (int)cl.block_rank() : 0;
+  const int seg = split ? blockIdx.x >> 1 : blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0 && crank == 0) SL_LSTAMP(7);  // kernel entry
+  if (split) {
+    if (tid == 0) {
+      sm.agg_ready = 0;
+      sm.inv_ready = 0;
+      sm.vbs_ready = 0;
+    }
+    cl.sync();  // both CTAs started, flags cleared, before any DSMEM store
+  }
+  LargeSmem* res = split ? cl.map_shared_rank(&sm, 0) : &sm;  // where fold results go
   const sl_cost& C = cfg.cost;
   const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -313,8 +343,32 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   int32_t* kept_list = out.scratch + wb;
   const bool need_inv = !guard_only && tpot_guard && R > 0 && W > 0;
   const bool need_vbs = !guard_only && R > 0;
-  if (tid == 0) SL_LSTAMP(0);
+  if (tid == 0 && crank == 0) SL_LSTAMP(0);
 
+  if (split && crank == 1 && warp < kLW) {
+    // CTA 1's spare warps: pull the segment's inputs into L2 (128-byte lines)
+    // so that neither the walk's gathers nor the folds' streams wait on HBM
+    const int nt = kLW * 32;
+    auto pf = [&](const void* base, int64_t bytes) {
+      const char* b = static_cast<const char*>(base);
+      for (int64_t o = (int64_t)tid * 128; o < bytes; o += (int64_t)nt * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b + o));
+    };
+    pf(st.r_tpot + rb, 8 * (int64_t)R);
+    pf(st.r_cur_len + rb, 4 * (int64_t)R);
+    pf(st.w_arrival + wb, 8 * (int64_t)W);
+    pf(st.w_prefill + wb, 8 * (int64_t)W);
+    pf(st.w_ttft + wb, 8 * (int64_t)W);
+    if (ttft_guard) pf(out.perm + wb, 4 * (int64_t)W);
+    pf(st.w_tpot + wb, 8 * (int64_t)W);
+    pf(st.w_prompt + wb, 4 * (int64_t)W);
+    pf(st.w_pred + wb, 4 * (int64_t)W);
+    return;
+  }
+  if (split && (crank == 0) == (warp >= kLW)) return;  // the other CTA's role
+  // named-barrier counts: warp 0 takes part in the aggregate / vbs barriers
+  // unless it polls CTA 0's flags instead (split)
+  const int agg_cnt = 5 * 32, vbs_cnt = split ? 2 * 32 : 3 * 32;
   if (warp >= kLW) {
     // ------------------------------------------------------------ fold warps
     if (guard_only) return;  // warp 0 waits on none of their barriers
@@ -329,14 +383,19 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
         if (f == 1) {
           const double fs = split_fold_f(R, tp, [](double t) { return frcp_(t); }, sm.sf[0],
                                          kBarInvRing, lane);
-          if (lane == 0) sm.inv_f = fs;
+          if (lane == 0) res->inv_f = fs;
         } else {
           const double cs = split_fold_c(R, sm.sf[0], kBarInvRing, sm.ebuf[0], lane);
-          if (lane == 0) sm.inv_c = cs;
+          if (lane == 0) res->inv_c = cs;
         }
       }
       if (f == 1) SL_LSTAMP(2);
-      bar_arrive(kBarAgg, 5 * 32);
+      if (split) {  // the inv pair alone: the min / lengths warps do not wait for it
+        bar_sync(kBarInvPair, 64);
+        if (f == 1 && lane == 0) flag_release(&res->inv_ready);
+      } else {
+        bar_arrive(kBarAgg, agg_cnt);
+      }
       return;
     }
     // vbs pair: min slo and sum of lengths over running
@@ -357,22 +416,31 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     bar_sync(kBarRed, 64);
     const double min_pre = fmin(sm.red_min[0], sm.red_min[1]);
     if (f == 3 && lane == 0) {
-      sm.min_pre = min_pre;
-      sm.lens = sm.red_len[0] + sm.red_len[1];
+      res->min_pre = min_pre;
+      res->lens = sm.red_len[0] + sm.red_len[1];
     }
     if (f == 3) SL_LSTAMP(3);
-    bar_arrive(kBarAgg, 5 * 32);
+    if (split) {
+      if (f == 3 && lane == 0) flag_release(&res->agg_ready);  // min / lengths
+    } else {
+      bar_arrive(kBarAgg, agg_cnt);
+    }
     if (need_vbs) {  // vbs over running with the pre-admission minimum (:312-315)
       if (f == 3) {
         const double fs = split_fold_f(R, tp, [&](double t) { return fdiv_(min_pre, t); },
                                        sm.sf[1], kBarVbsRing, lane);
-        if (lane == 0) sm.vbs_f = fs;
+        if (lane == 0) res->vbs_f = fs;
         SL_LSTAMP(4);
       } else {
         const double cs = split_fold_c(R, sm.sf[1], kBarVbsRing, sm.ebuf[1], lane);
-        if (lane == 0) sm.vbs_c = cs;
+        if (lane == 0) res->vbs_c = cs;
       }
-      bar_arrive(kBarVbs, 3 * 32);  // warp 0 waits on it iff R > 0
+      if (split) {
+        bar_sync(kBarVbs, vbs_cnt);
+        if (f == 3 && lane == 0) flag_release(&res->vbs_ready);
+      } else {
+        bar_arrive(kBarVbs, vbs_cnt);  // warp 0 waits on it iff R > 0
+      }
     }
     return;
   }
@@ -506,6 +574,15 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       if (warp == 0) {
         const double P1 = survivor_chain(sm, sm.n_sv, P0, lane);
         if (lane == 0) sm.P = P1;
+      } else {
+        // while warp 0 runs the chain: pull the next tile's inputs into L2 (the
+        // walk order gathers them through perm, two dependent round trips cold)
+        for (int p = t0 + kLTile + tid - 32; p < min(W, t0 + 2 * kLTile); p += kLWalkThreads - 32) {
+          const int32_t q = qidx(p);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(st.w_arrival + q));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(st.w_prefill + q));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(st.w_ttft + q));
+        }
       }
       bar_sync(kBarWalk, kLWalkThreads);
 #ifdef SL_LARGE_PROF
@@ -579,7 +656,12 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   if (warp != 0) return;
 
   // ---------------------------------------------------- admission (warp 0)
-  bar_sync(kBarAgg, 5 * 32);
+  if (split) {
+    flag_acquire(&sm.agg_ready);
+    flag_acquire(&sm.inv_ready);
+  } else {
+    bar_sync(kBarAgg, agg_cnt);
+  }
   int64_t lens = sm.lens;
   double min_d = sm.min_pre;
   const double min_pre = min_d;
@@ -681,7 +763,12 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   if (has_min) {
     PySum vs;
     int j0 = 0;  // first entry (running then admitted) still to fold
-    if (R > 0) bar_sync(kBarVbs, 3 * 32);
+    if (R > 0) {
+      if (split)
+        flag_acquire(&sm.vbs_ready);
+      else
+        bar_sync(kBarVbs, vbs_cnt);
+    }
     if (R > 0 && min_d == min_pre) {
       vs = {sm.vbs_f, sm.vbs_c, 1};  // the vbs pair folded the running part with this minimum
       j0 = R;
