@@ -88,6 +88,37 @@ def test_sharded_nccl_two_gpus_bit_identical_to_unsharded():
     _run("nccl")
 
 
+def _nccl_one_rank(port, q):
+    import torch.distributed as dist
+
+    from paper_2505_23022_b200.sweep import build_local, gather_rows
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    grid = _grid(1)
+    eng, owned, _ = build_local(grid, 0, 1, device=dev)
+    eng.launch()
+    torch.cuda.synchronize()
+    full = gather_rows(eng.results_device(), owned, grid.n_cells)  # NCCL on device tensors
+    q.put((full.tobytes(), eng.results().tobytes()))
+    dist.destroy_process_group()
+
+
+def test_gather_rows_over_nccl_on_device_tensors():
+    """The NCCL all_gather path of gather_rows (what bench.py runs at N > 1), on the
+    one GPU this lease has: a single-rank NCCL group gathers the device rows."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_one_rank, args=(32000 + os.getpid() % 1000, q))
+    p.start()
+    full, want = q.get(timeout=300)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert full == want
+
+
 def test_bench_refuses_more_gpus_than_visible():
     n = torch.cuda.device_count() + 1
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n),
