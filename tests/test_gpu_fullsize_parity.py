@@ -5,11 +5,12 @@
   requests, compliant <= completed, violation counts <= completed, goodput ==
   compliant / sim_end, adherence == compliant / total, no engine error, request
   steps >= steps);
+* every one of the 4,096 cells (and of config 4's 16,384): every result-row
+  field and the work-step digest bit-exact against the C oracle on the same
+  traces;
 * 48 stratified cells (every rate row, scales spread over the axis, the 2 req/s
-  critical-path cells included): every result-row field, the work-step digest
-  and every request's outcome (status, completion step, first-token and
-  completion times, TTFT, TPOT, compliance) bit-exact against the C oracle on
-  the same traces.
+  critical-path cells included): also every request's outcome (status,
+  completion step, first-token and completion times, TTFT, TPOT, compliance).
 """
 
 OUTCOME_FIELDS = ("status", "compliant", "completion_step", "first_token_time",
@@ -93,6 +94,40 @@ def test_config3_sampled_cells_match_oracle(config3):
         assert_outcomes_equal(eng.cell_outcomes(ri * ns + si), ref, (ri, si))
 
 
+def _all_cells_vs_oracle(res, traces, scales, config, batch=256):
+    """Every cell's result row and work-step digest against the C oracle on the
+    same traces (outcome arrays are dropped per batch to bound host memory)."""
+    from oracle import oracle as orc
+
+    params = orc.make_params(itl=config.itl, prefill=config.prefill)
+    ns = len(scales)
+    cells = [(ri, si) for ri in range(len(traces)) for si in range(ns)]
+    for b in range(0, len(cells), batch):
+        chunk = cells[b:b + batch]
+        jobs = []
+        for ri, si in chunk:
+            t, s = traces[ri], float(scales[si])
+            jobs.append(dict(arrival=t.arrival, ttft_slo=t.ttft_slo * s, tpot_slo=t.tpot_slo * s,
+                             prompt_len=t.prompt_len, true_out=t.true_out, ids=t.id,
+                             predicted=t.predicted, params=params))
+        for (ri, si), ref in zip(chunk, orc.run_many(jobs)):
+            r, sm = res[ri * ns + si], ref["summary"]
+            assert ref["rc"] == 0
+            for f in FIELDS:
+                assert r[f] == sm[f], (ri, si, f, r[f], sm[f])
+            for f in ("sim_end", "goodput", "adherence"):
+                assert same_float([r[f]], [sm[f]]), (ri, si, f)
+            assert int(r["digest"]) == sm["digest"], (ri, si)
+
+
+def test_config3_every_cell_matches_oracle(config3):
+    """All 4,096 cells of the bench workload: every result-row field (counts,
+    request-steps, sim_end, goodput, adherence) and the work-step digest --
+    every admit / reject / batch decision and step end time -- bit-exact."""
+    grid, res, traces, _ = config3
+    _all_cells_vs_oracle(res, traces, grid.scales, grid.config)
+
+
 def test_config4_sampled_cells_match_oracle():
     """Config 4 at full size (16,384 ShareGPT-shaped sims with the device
     noisy-bucket predictor in the loop -- its stream is pinned to numpy's in
@@ -142,3 +177,5 @@ def test_config4_sampled_cells_match_oracle():
             assert r[f] == sm[f], (ri, si, f, r[f], sm[f])
         assert same_float([r["goodput"]], [sm["goodput"]]) and int(r["digest"]) == sm["digest"]
         assert_outcomes_equal(eng.cell_outcomes(ri * 128 + si), ref, (ri, si))
+    # and every one of the 16,384 cells: result row + work-step digest
+    _all_cells_vs_oracle(res, traces, grid.scales, grid.config)
