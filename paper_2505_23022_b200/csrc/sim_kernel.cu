@@ -20,6 +20,8 @@
 //    (one chunk load per 32 items, values broadcast with shuffles) so every
 //    lane holds the same state and no lane diverges.
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
@@ -879,29 +881,47 @@ int sl_run_batch_ex(const sl_traces* traces, const sl_sim* sims, const int32_t* 
     wrec_prepass_kernel<<<grid, 256, 0, st>>>(a);
     if (cudaGetLastError() != cudaSuccess) return SL_ERR_CUDA;
   }
-  int dev = 0, sms = 0;
+  // launch geometry per device, queried once (SM count, resident blocks per SM of
+  // each kernel; the SL_* experiment knobs read once too) -- no per-call queries
+  constexpr int kMaxDev = 64;
+  static int geo_sms[kMaxDev], geo_per_sm[kMaxDev][4];
+  static std::atomic<bool> geo_ok[kMaxDev];
+  static const int env_cap = [] {
+    const char* e = getenv("SL_BLOCKS_PER_SM");  // experiments: cap residency
+    return e ? atoi(e) : 0;
+  }();
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto grid_for = [&](const void* fn, int threads) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
-    if (const char* e = getenv("SL_BLOCKS_PER_SM")) {  // experiments: cap residency
-      int cap = atoi(e);
-      if (cap > 0 && cap < per_sm) per_sm = cap;
+  const void* fns[4] = {(const void*)sl_sim_fast_kernel<true, false>,
+                        (const void*)sl_sim_fast_kernel<true, true>,
+                        (const void*)sl_sim_fast_kernel<false, false>, (const void*)sl_sim_kernel};
+  const int fthreads[4] = {32 * kFastWarps, 32 * kFastWarps, 32 * kFastWarps, 128};
+  if (dev < 0 || dev >= kMaxDev) return SL_ERR_ARG;
+  if (!geo_ok[dev].load(std::memory_order_acquire)) {  // (racing first calls compute the same)
+    if (const char* e = getenv("SL_CARVEOUT")) {  // experiments: shared-memory carveout (percent)
+      const int pct = atoi(e);
+      cudaFuncSetAttribute(fns[0], cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      cudaFuncSetAttribute(fns[1], cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     }
-    if (per_sm < 1) per_sm = 1;
+    cudaDeviceGetAttribute(&geo_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    for (int k = 0; k < 4; ++k) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[k], fthreads[k], 0);
+      if (env_cap > 0 && env_cap < per_sm) per_sm = env_cap;
+      geo_per_sm[dev][k] = per_sm < 1 ? 1 : per_sm;
+    }
+    geo_ok[dev].store(true, std::memory_order_release);
+  }
+  const int sms = geo_sms[dev];
+  auto grid_for = [&](const void* fn, int threads) {
+    int per_sm = 1;
+    for (int k = 0; k < 4; ++k)
+      if (fns[k] == fn) per_sm = geo_per_sm[dev][k];
     int64_t wpb = threads / 32;
     int64_t blocks = (n_sims + wpb - 1) / wpb;
     int64_t max_blocks = (int64_t)sms * per_sm;
     return (unsigned)(blocks < max_blocks ? blocks : max_blocks);
   };
-  if (const char* e = getenv("SL_CARVEOUT")) {  // experiments: shared-memory carveout (percent)
-    const int pct = atoi(e);
-    cudaFuncSetAttribute((const void*)sl_sim_fast_kernel<true, false>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute((const void*)sl_sim_fast_kernel<true, true>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  }
   if (mode == SL_MODE_AUTO) {
     if (!a.has_log) {
       if (a.has_out)
