@@ -25,6 +25,12 @@ constexpr int kRunCap = 32 * kSlots;
 #ifndef SL_INV_UNROLL
 #define SL_INV_UNROLL 0  // unrolled branch-free 1/slo fold (measured: 112 -> 118 ms, registers)
 #endif
+#ifndef SL_QUIET_SMEM
+#define SL_QUIET_SMEM 1  // quiet loop: per-step digest inputs in a shared-memory ring
+#endif
+#ifndef SL_QUIET_NOLIVE
+#define SL_QUIET_NOLIVE 0  // quiet loop: dead lanes neutralised once instead of tested per step
+#endif
 #ifndef SL_ACC_SMEM
 #define SL_ACC_SMEM 0  // per-lane outcome counters in shared memory instead of registers
 #endif
@@ -681,6 +687,70 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
       }
     }
   }
+#elif SL_QUIET_SMEM
+  // the step's digest inputs (batch size, batch hash, end time) go to a 32-entry
+  // ring in the (here unused) scratch: one lane's store per step, hashed 32 steps
+  // at a time lane-parallel
+  uint4* ring = reinterpret_cast<uint4*>(scr);
+  int flushed = 0;  // steps [0, flushed) of this call are hashed
+#if SL_QUIET_NOLIVE
+  // lanes past R hold no entry: zero credit, earn 0, S = 1 -> never batched, and
+  // rem = 1 -> never retire, so the step needs no liveness tests (their slot
+  // fields are dead and are overwritten by put_slot when an entry arrives)
+  const cred_t<WIDE> earn = live ? g.Smin : cred_t<WIDE>(0);
+  if (!live) {
+    sl[0].N = 0;
+    sl[0].S = 1;
+    sl[0].rem = 1;
+  }
+#endif
+  while (R > 0 && R <= 32 && now < lim) {
+#if SL_QUIET_NOLIVE
+    const cred_t<WIDE> N = sl[0].N + earn;
+    const bool b = all ? live : N >= sl[0].S;  // all: decode-all policies, no credits
+    if (!all) sl[0].N = b ? N - sl[0].S : N;
+#else
+    const cred_t<WIDE> N = sl[0].N + g.Smin;
+    const bool b = live && (all || N >= sl[0].S);  // all: decode-all policies, no credits
+    if (live && !all) sl[0].N = b ? N - sl[0].S : N;
+#endif
+    const int nb = __popc(__ballot_sync(SL_FULL, b));
+    const unsigned blen = __reduce_add_sync(SL_FULL, b ? (unsigned)sl[0].cur_len : 0u);
+    const unsigned bh = __reduce_add_sync(SL_FULL, b ? hh : 0u);
+    if (b) {
+      sl[0].cur_len += 1;
+      sl[0].rem -= 1;
+    }
+    const double end = fadd_(now, itl(C, nb, div_small((double)blen, nb)));
+    if (lane == (k & 31)) {
+      const uint64_t eb = (uint64_t)__double_as_longlong(end);
+      ring[k & 31] = make_uint4((unsigned)nb, bh, (unsigned)eb, (unsigned)(eb >> 32));
+    }
+#if SL_QUIET_NOLIVE
+    ret = __any_sync(SL_FULL, sl[0].rem <= 0);
+#else
+    ret = __any_sync(SL_FULL, live && sl[0].rem <= 0);
+#endif
+    now = end;
+    ++k;
+    if (ret) break;
+    if ((k & 31) == 0) {
+      __syncwarp();
+      const uint4 q = ring[lane];
+      const uint64_t st = (uint64_t)(step0 + k - 32 + lane);
+      acc.dig += digest_item(st, 2, q.x, q.y) +
+                 digest_item(st, 3, 0, ((uint64_t)q.w << 32) | q.z);
+      flushed = k;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  if (flushed + lane < k) {
+    const uint4 q = ring[lane];
+    const uint64_t st = (uint64_t)(step0 + flushed + lane);
+    acc.dig += digest_item(st, 2, q.x, q.y) + digest_item(st, 3, 0, ((uint64_t)q.w << 32) | q.z);
+  }
+  __syncwarp();
 #else
   while (R > 0 && R <= 32 && now < lim) {
     const cred_t<WIDE> N = sl[0].N + g.Smin;
