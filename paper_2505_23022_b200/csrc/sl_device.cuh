@@ -17,6 +17,10 @@
 
 #define SL_FULL 0xffffffffu
 
+#ifndef SL_PSADD_SEL
+#define SL_PSADD_SEL 0  // CPython sum() step: select the operands, then one error expression
+#endif
+
 namespace sl {
 
 __device__ __forceinline__ double fadd_(double a, double b) { return __dadd_rn(a, b); }
@@ -66,7 +70,14 @@ __device__ __forceinline__ void ps_add(PySum& s, double x) {
     s.n = 1;
   } else {
     double t = fadd_(s.f, x);
+#if SL_PSADD_SEL
+    // operands selected first, one error expression (2 DADDs, not 4 + a select)
+    const bool big = fabs(s.f) >= fabs(x);
+    const double hi = big ? s.f : x, lo = big ? x : s.f;
+    double a = fadd_(fsub_(hi, t), lo);
+#else
     double a = (fabs(s.f) >= fabs(x)) ? fadd_(fsub_(s.f, t), x) : fadd_(fsub_(x, t), s.f);
+#endif
     s.c = fadd_(s.c, a);
     s.f = t;
   }
