@@ -341,12 +341,14 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
     alone on the stream (enqueued behind a GPU sleep so no host launch overhead
     is timed), L2 flushed before each.  Compulsory bytes (each input read once,
     each output written once): sort 16 B read (arrival, ttft: the deadline key;
-    the id is read only on deadline ties) + 4 B written (perm) per waiting item; scan 44 B read (perm, arrival, prefill, ttft, tpot,
-    prompt, predicted) + 8 B written (status, position) per waiting item and 12 B
-    read (tpot, current length) per running item (admission records of admitted
-    items not counted); select 17 B read (tpot, credit, exclude) + 13 B written
-    (credit, batch flag, position) per running item; fused = the union without the
-    perm round trip (48 + 12 B per waiting item, 21 + 13 B per running item)."""
+    the id is read only on deadline ties) + 4 B written (perm) per waiting item;
+    scan 44 B read (perm, arrival, prefill, ttft, tpot, prompt, predicted) + 8 B
+    written (status, position) per waiting item, 12 B read (tpot, current
+    length) per running item, 40 B written per admitted item (its
+    AdmissionRecord inputs) and per segment (counts, vbs, min_slo, fixed-point
+    minimum); select 17 B read (tpot, credit, exclude) + 13 B written (credit,
+    batch flag, position) per running item; fused = the union without the perm
+    round trip (48 + 12 B per waiting item, 21 + 13 B per running item)."""
     import torch
 
     from paper_2505_23022_b200.plan import PlanBatch
@@ -381,8 +383,12 @@ def plan_microbench(dev, peak: float, reps: int = 5) -> dict:
                 torch.cuda.synchronize()
                 if it >= 2:
                     times[k].append(e0.elapsed_time(e1) / 1e3)
-        bytes_ = {"sort": 20 * Wt, "scan": 52 * Wt + 12 * Rt, "select": 30 * Rt,
-                  "fused": 60 * Wt + 34 * Rt}
+        # admitted items also write their AdmissionRecord inputs (5 doubles:
+        # V, L, min', estimate, threshold -- sched_scorpio.py:254-271)
+        n_adm = int(pb.o["seg_counts"].view(-1, 4)[:, 1].sum().item())
+        # + 40 B of per-segment results (counts, vbs, min_slo, fixed-point min)
+        bytes_ = {"sort": 20 * Wt, "scan": 52 * Wt + 12 * Rt + 40 * n_adm + 40 * S,
+                  "select": 30 * Rt, "fused": 60 * Wt + 34 * Rt + 40 * n_adm + 40 * S}
         rows = {}
         for k in phases:
             t = float(np.mean(times[k]))

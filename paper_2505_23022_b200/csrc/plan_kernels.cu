@@ -216,7 +216,8 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
                                                 const sl_plan_out& out, int seg, int lane,
                                                 double inv_pre = 0.0, double* min_out = nullptr,
                                                 bool* has_min_out = nullptr,
-                                                int* nadm_out = nullptr) {
+                                                int* nadm_out = nullptr,
+                                                int32_t* klist32 = nullptr) {
   const sl_cost& C = cfg.cost;
   const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -232,7 +233,9 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   const double now = st.now[seg];
   const int E = st.credit_exp[seg];
   const double pow2E = __longlong_as_double((long long)(E + 1023) << 52);
-  int32_t* kept_list = out.scratch + wb;
+  // the walk's kept list: the warp's 32-entry shared buffer for segments of <= 32
+  // waiting (no global round trip), else the segment's slice of out.scratch
+  int32_t* kept_list = (klist32 && W <= 32) ? klist32 : out.scratch + wb;
   int nrej = 0, kept = 0;
 
   // 1. TTFT walk over the LDF order (speculative-parallel, exact), or the FCFS queue.
@@ -517,9 +520,11 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
 
 __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config cfg,
                                    sl_plan_out out) {
+  __shared__ int32_t klist[32][32];  // per warp (blockDim <= 1024)
   const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (seg >= st.n_segments) return;
-  seg_guard_admit(st, cfg, out, seg, threadIdx.x & 31);
+  seg_guard_admit(st, cfg, out, seg, threadIdx.x & 31, 0.0, nullptr, nullptr, nullptr,
+                  klist[threadIdx.x >> 5]);
 }
 
 // Large batches: one warp per kPlanGroup segments.  The order-dependent Neumaier folds
@@ -536,6 +541,7 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
 constexpr int kPlanGroup = SL_PLAN_GROUP;
 __global__ void __launch_bounds__(128, SL_PLAN_GROUP_BLOCKS) guard_admit_group_kernel(
     const sl_plan_state st, const sl_plan_config cfg, sl_plan_out out) {
+  __shared__ int32_t klist[4][32];  // per warp (128 threads)
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int seg0 = warp * kPlanGroup;
@@ -561,7 +567,8 @@ __global__ void __launch_bounds__(128, SL_PLAN_GROUP_BLOCKS) guard_admit_group_k
     bool h_k = false;
     int a_k = 0;
     seg_guard_admit<true>(st, cfg, out, seg0 + k, lane, __shfl_sync(SL_FULL, inv, k), &m_k, &h_k,
-                          &a_k);
+                          &a_k, klist[threadIdx.x >> 5]);
+    __syncwarp();  // the next segment reuses the warp's kept-list buffer
     if (lane == k) {
       min_d = m_k;
       has_min = h_k;

@@ -28,6 +28,9 @@ constexpr int kRunCap = 32 * kSlots;
 #ifndef SL_QUIET_SMEM
 #define SL_QUIET_SMEM 1  // quiet loop: per-step digest inputs in a shared-memory ring
 #endif
+#ifndef SL_ARR2
+#define SL_ARR2 0  // keep the arrival time after next in a register (single-arrival fast path)
+#endif
 #ifndef SL_QUIET_NOLIVE
 #define SL_QUIET_NOLIVE 0  // quiet loop: dead lanes neutralised once instead of tested per step
 #endif
@@ -891,6 +894,11 @@ __device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, i
   double now = 0.0;
   int64_t next = 0;
   double next_t = n > 0 ? s.wr[0].arr : kInf;  // WRec built by wrec_prepass_kernel
+#if SL_ARR2
+  // the arrival after next, so that the common single arrival needs no load on
+  // the step's path (the next one is then already known)
+  double next_t2 = n > 1 ? s.wr[1].arr : kInf;
+#endif
   int W = 0, R = 0;
   int64_t step = 0, n_plans = 0, n_idle = 0, req_steps = 0;
   int status = SL_SIM_OK;
@@ -904,7 +912,24 @@ __device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, i
   for (;;) {
     if (next < n && next_t <= now) {
       const int64_t n0 = next;
+#if SL_ARR2
+      if (next_t2 > now && (sorted_ldf || sjf)) {  // exactly one request arrives
+        insert_sorted(s, W, (int)next, sjf, lane);
+        ++next;
+        next_t = next_t2;
+        next_t2 = next + 1 < n ? (s.factor == 1.0 ? s.arrival[next + 1] : s.wr[next + 1].arr)
+                               : kInf;
+#if SL_PREFETCH
+        if (lane == 0 && next < n) asm volatile("prefetch.global.L1 [%0];" ::"l"(s.wr + next));
+#endif
+      } else {
+        process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
+        next_t2 = next + 1 < n ? (s.factor == 1.0 ? s.arrival[next + 1] : s.wr[next + 1].arr)
+                               : kInf;
+      }
+#else
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
+#endif
       arrivals_keep_bounds(s, n0, (int)(next - n0), now, ttft_guard, blocked, walk_until, p_up,
                            lane);
     }
