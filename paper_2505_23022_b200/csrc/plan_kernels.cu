@@ -762,6 +762,126 @@ __global__ void __launch_bounds__(kSelCta) credit_select_cta_kernel(const sl_pla
 // Segment count below which credit select runs one CTA per segment.
 constexpr int kSelCtaMaxSegments = 64;
 
+// Credit select for few, large segments over a cluster of kSelCluster CTAs per
+// segment: CTA q takes the q-th contiguous slice of the running list.  Pass 1:
+// every entry's credit update and batch flag (written out), the slice's batch
+// count; the counts (and, without a given minimum, the slices' minima first)
+// are pushed into every CTA's shared memory with one cluster barrier each; pass
+// 2: batch positions from the count of the slices before this one plus a
+// blocked ballot scan over the slice (the flags re-read from r_batch).
+constexpr int kSelCluster = 8;
+__device__ __forceinline__ int cta_excl_scan_i(int v, int* wtot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(SL_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = wtot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(SL_FULL, t, o);
+      if (lane >= o) t += y;
+    }
+    wtot[lane] = t;  // inclusive
+  }
+  __syncthreads();
+  const int r = (w ? wtot[w - 1] : 0) + x - v;
+  return r;
+}
+
+__global__ void __launch_bounds__(kSelCta) credit_select_cluster_kernel(const sl_plan_state st,
+                                                                        const sl_plan_config cfg,
+                                                                        sl_plan_out out,
+                                                                        int use_seg_min) {
+  namespace cg = cooperative_groups;
+  __shared__ int wtot[32];
+  __shared__ unsigned long long cmin[kSelCluster];  // pushed by every CTA
+  __shared__ int ctot[kSelCluster];
+  __shared__ unsigned long long smin;
+  __shared__ int lcount;
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int seg = blockIdx.x / kSelCluster;
+  const int tid = threadIdx.x;
+  const bool credit = cfg.flags & SL_FLAG_TPOT_GUARD;
+  const int64_t rb = st.r_begin[seg];
+  const int R = (int)(st.r_begin[seg + 1] - rb);
+  const int E = st.credit_exp[seg];
+  const int chunk = (R + kSelCluster - 1) / kSelCluster;
+  const int lo = min(R, q * chunk), hi = min(R, lo + chunk);
+  if (tid == 0) {
+    smin = ~0ull;
+    lcount = 0;
+  }
+  cl.sync();  // every CTA started (DSMEM stores below), locals initialised
+  uint64_t MIN = ~0ull;
+  if (credit) {
+    if (use_seg_min) {
+      MIN = out.seg_min_fixed[seg];
+    } else {  // min fixed-point slo over the whole running list
+      uint64_t m = ~0ull;
+      for (int j = lo + tid; j < hi; j += kSelCta) {
+        const uint64_t S = slo_fixed<false>(st.r_tpot[rb + j], E);
+        m = S < m ? S : m;
+      }
+      m = warp_min_cred<false>(m);
+      if ((tid & 31) == 0) atomicMin(&smin, (unsigned long long)m);
+      __syncthreads();
+      if (tid < kSelCluster) cl.map_shared_rank(cmin, tid)[q] = smin;
+      cl.sync();
+      for (int k = 0; k < kSelCluster; ++k) MIN = min(MIN, (uint64_t)cmin[k]);
+    }
+  }
+  // pass 1: credits and batch flags of this slice
+  int cnt = 0;
+  for (int j = lo + tid; j < hi; j += kSelCta) {
+    const int64_t r = rb + j;
+    const bool ex = st.r_exclude && st.r_exclude[r];
+    uint64_t N = st.r_credit[r];
+    bool b = false;
+    if (!ex) {
+      if (credit) {
+        const uint64_t S = slo_fixed<false>(st.r_tpot[r], E);
+        N += MIN;
+        b = N >= S;
+        if (b) N -= S;
+      } else {
+        b = true;
+      }
+    }
+    out.r_credit_out[r] = N;
+    out.r_batch[r] = b;
+    cnt += b;
+  }
+  cnt = __reduce_add_sync(SL_FULL, (unsigned)cnt);
+  if ((tid & 31) == 0) atomicAdd(&lcount, cnt);
+  __syncthreads();
+  if (tid < kSelCluster) cl.map_shared_rank(ctot, tid)[q] = lcount;
+  cl.sync();  // every slice's count everywhere; r_batch written (block-scope visibility below)
+  int base = 0, total = 0;
+  for (int k = 0; k < kSelCluster; ++k) {
+    base += k < q ? ctot[k] : 0;
+    total += ctot[k];
+  }
+  // pass 2: positions, 1024 entries per round in slice order
+  for (int j0 = lo; j0 < hi; j0 += kSelCta) {
+    const int j = j0 + tid;
+    const bool b = j < hi && out.r_batch[rb + j];
+    const int e = cta_excl_scan_i(b ? 1 : 0, wtot);
+    if (j < hi) out.r_pos[rb + j] = b ? base + e : -1;
+    base += wtot[31];
+    __syncthreads();  // wtot reused by the next round
+  }
+  if (q == 0 && tid == 0) out.seg_counts[4 * seg + 3] = total;
+}
+
+
+
 // ---- plan_step of one segment with <= 32 waiting and <= 32 running, all in
 // registers (the config-2 primary shape).  Every input of the segment is loaded
 // up front -- one memory latency instead of one per stage -- and the stages
@@ -1251,6 +1371,24 @@ int sl_credit_select_batch(const sl_plan_state* st, const sl_plan_config* cfg, s
       !out->seg_counts || (use_seg_min && !out->seg_min_fixed))
     return SL_ERR_ARG;
   if (st->n_segments == 0) return SL_OK;
+  const char* ce = getenv("SL_SELECT_CLUSTER");
+  if (st->n_segments <= kSelCtaMaxSegments && !(ce && ce[0] == '0')) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(st->n_segments * kSelCluster);
+    lc.blockDim = dim3(kSelCta);
+    lc.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kSelCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, credit_select_cluster_kernel, *st, *cfg, *out, use_seg_min) !=
+        cudaSuccess)
+      return SL_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+  }
   if (st->n_segments <= kSelCtaMaxSegments)
     credit_select_cta_kernel<<<st->n_segments, kSelCta, 0, (cudaStream_t)stream>>>(
         *st, *cfg, *out, use_seg_min);
