@@ -23,6 +23,10 @@
 
 using namespace sl;
 
+#ifndef SL_SORT32
+#define SL_SORT32 1  // warp LDF networks on 32-bit range-relative keys (near-ties: full keys)
+#endif
+
 namespace {
 
 constexpr int kTile = 2048;  // CTA sort tile
@@ -59,19 +63,67 @@ __device__ __forceinline__ Key inf_key() {
   return k;
 }
 
+// LDF order of <= 32 items held one per lane (deadline d >= 0, valid lanes <
+// n) by a bitonic network over 32-bit keys: the deadline's bit pattern minus the
+// warp minimum (monotone for non-negative doubles), shifted right so that the
+// range fits 27 bits, with the lane (input position) in the low 5 bits.
+// Returns the input lane at this lane's sorted position, or -1 when two
+// adjacent sorted keys share their top 27 bits (equal or near-equal deadlines:
+// the caller falls back to a full-key network).
+__device__ __forceinline__ int warp_ldf_src32(double d, bool valid, int n, int lane) {
+  const uint64_t b = valid ? (uint64_t)__double_as_longlong(d) : 0ull;
+  const unsigned hmin = __reduce_min_sync(SL_FULL, valid ? (unsigned)(b >> 32) : ~0u);
+  const unsigned lmin = __reduce_min_sync(SL_FULL, valid && (unsigned)(b >> 32) == hmin
+                                                       ? (unsigned)b : ~0u);
+  const uint64_t bmin = ((uint64_t)hmin << 32) | lmin;
+  const uint64_t off = valid ? b - bmin : 0ull;
+  const unsigned ohi = __reduce_max_sync(SL_FULL, (unsigned)(off >> 32));
+  const unsigned olo = __reduce_max_sync(SL_FULL, (unsigned)(off >> 32) == ohi ? (unsigned)off : 0u);
+  const uint64_t omax = ((uint64_t)ohi << 32) | olo;
+  const int bits = omax ? 64 - __clzll((long long)omax) : 0;  // significant bits of the range
+  const int sh = bits > 27 ? bits - 27 : 0;
+  unsigned key = valid ? ((unsigned)(off >> sh) << 5) | (unsigned)lane : ~0u;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      const unsigned ok = __shfl_xor_sync(SL_FULL, key, j);
+      const bool up = (lane & size) == 0;
+      const bool lower = (lane & j) == 0;
+      key = ((lower == up) == (ok < key)) ? ok : key;
+    }
+  }
+  const unsigned next = __shfl_down_sync(SL_FULL, key, 1);
+  if (__any_sync(SL_FULL, lane + 1 < n && (next >> 5) == (key >> 5))) return -1;
+  return (int)(key & 31);
+}
+
 // ---- sort: one warp per segment (<= 32 items), bitonic network over shuffles
+// (d_pre: this lane's deadline when the caller has loaded it already -- the
+// grid-stride kernel pipelines the next segment's loads -- else loaded here)
 __device__ __forceinline__ void seg_sort_warp(const sl_plan_state& st, int32_t* perm, int seg,
-                                              int lane) {
+                                              int lane, const double* d_pre = nullptr) {
   const int64_t b = st.w_begin[seg];
   const int n = (int)(st.w_begin[seg + 1] - b);
   // Fast path: non-negative deadlines order like their bit patterns.  The
-  // network sorts one 64-bit key per lane -- the deadline bits with the low 5
-  // bits replaced by the lane (input position) -- one 64-bit shuffle per stage.
-  // Distinct keys in the top 59 bits make that the LDF order; otherwise (ties or
-  // near-ties, rare) the full (deadline, arrival, id) network below decides.
+  // network sorts one 32-bit key per lane (warp_ldf_src32: range-relative
+  // deadline bits, lane in the low 5 bits; SL_SORT32=0: the 64-bit form, the
+  // deadline bits with the low 5 bits replaced by the lane).  Distinct keys
+  // above the lane bits make that the LDF order; otherwise (ties or near-ties,
+  // rare) the full (deadline, arrival, id) network below decides.
   double d = 0.0;
-  if (lane < n) d = fadd_(st.w_arrival[b + lane], st.w_ttft[b + lane]);  // core.py:50-53
-  if (__all_sync(SL_FULL, lane >= n || d >= 0.0)) {
+  if (d_pre)
+    d = *d_pre;
+  else if (lane < n)
+    d = fadd_(st.w_arrival[b + lane], st.w_ttft[b + lane]);  // core.py:50-53
+  if (SL_SORT32 && __all_sync(SL_FULL, lane >= n || d >= 0.0)) {
+    const int src = warp_ldf_src32(d, lane < n, n, lane);
+    if (src >= 0) {
+      if (lane < n) perm[b + lane] = (int32_t)(b + src);
+      return;
+    }
+  }
+  if (!SL_SORT32 && __all_sync(SL_FULL, lane >= n || d >= 0.0)) {
     uint64_t key = lane < n ? (((uint64_t)__double_as_longlong(d) & ~31ull) | (uint64_t)lane)
                             : ~0ull;
 #pragma unroll
@@ -109,10 +161,30 @@ __device__ __forceinline__ void seg_sort_warp(const sl_plan_state& st, int32_t* 
   if (lane < n) perm[b + lane] = k.idx;
 }
 
+// grid-stride over segments: a bounded grid (resident warps) instead of one
+// 4-warp block per 4 segments, so block launches do not pace large batches
 __global__ void sort_warp_kernel(const sl_plan_state st, int32_t* perm) {
-  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (seg >= st.n_segments) return;
-  seg_sort_warp(st, perm, seg, threadIdx.x & 31);
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // the next segment's deadline inputs are in flight while this one is sorted
+  auto fetch = [&](int sg, double& a, double& t) {
+    a = t = 0.0;
+    if (sg < st.n_segments) {
+      const int64_t b = st.w_begin[sg];
+      if (lane < st.w_begin[sg + 1] - b) {
+        a = st.w_arrival[b + lane];
+        t = st.w_ttft[b + lane];
+      }
+    }
+  };
+  double a_n, t_n;
+  fetch(seg, a_n, t_n);
+  for (; seg < st.n_segments; seg += nw) {
+    const double d = fadd_(a_n, t_n);  // core.py:50-53 (unused past the segment's end)
+    fetch(seg + nw, a_n, t_n);
+    seg_sort_warp(st, perm, seg, lane, &d);
+  }
 }
 
 // ---- sort: one CTA per (segment, tile of <= kTile items), bitonic over smem
@@ -647,9 +719,9 @@ __device__ __forceinline__ void seg_credit_select(const sl_plan_state& st,
 
 __global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_config cfg,
                                      sl_plan_out out, int use_seg_min) {
-  const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (seg >= st.n_segments) return;
-  seg_credit_select(st, cfg, out, use_seg_min, seg, threadIdx.x & 31);
+  const int nw = (gridDim.x * blockDim.x) >> 5;  // grid-stride, as sort_warp_kernel
+  for (int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < st.n_segments; seg += nw)
+    seg_credit_select(st, cfg, out, use_seg_min, seg, threadIdx.x & 31);
 }
 
 // Few, large segments (the config-2 stress shape): one 1024-thread CTA per
@@ -1230,6 +1302,21 @@ __global__ void vbs_kernel(int S, const int64_t* r_begin, const double* r_tpot,
 
 int warps_grid(int n_warps, int threads) { return (n_warps * 32 + threads - 1) / threads; }
 
+// Grid for the grid-stride warp-per-segment kernels: at most `per_sm` blocks
+// per SM (SL_STRIDE_BLOCKS overrides for experiments).
+int stride_grid(int n_warps, int threads, int per_sm) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (const char* e = getenv("SL_STRIDE_BLOCKS")) per_sm = atoi(e);
+  const int need = warps_grid(n_warps, threads);
+  const int cap = sms * per_sm;
+  return need < cap ? need : cap;
+}
+
 // Segment count from which guard_admit uses the 32-segments-per-warp kernel
 // (enough groups to fill the GPU); SL_PLAN_GROUP_MIN overrides it (tests force
 // either path).  The fused single-launch plan step is used below it.
@@ -1273,7 +1360,7 @@ int sl_ttft_sort_batch(const sl_plan_state* st, int64_t max_w, sl_plan_out* out,
   if (S == 0 || max_w == 0) return SL_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (max_w <= 32) {
-    sort_warp_kernel<<<warps_grid(S, 128), 128, 0, s>>>(*st, out->perm);
+    sort_warp_kernel<<<stride_grid(S, 128, 32), 128, 0, s>>>(*st, out->perm);
     return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
   }
   if (S <= plan_cta_max() && max_w <= kSortMaxCluster * kSortLoc) {  // few large segments
@@ -1393,7 +1480,7 @@ int sl_credit_select_batch(const sl_plan_state* st, const sl_plan_config* cfg, s
     credit_select_cta_kernel<<<st->n_segments, kSelCta, 0, (cudaStream_t)stream>>>(
         *st, *cfg, *out, use_seg_min);
   else
-    credit_select_kernel<<<warps_grid(st->n_segments, 128), 128, 0, (cudaStream_t)stream>>>(
+    credit_select_kernel<<<stride_grid(st->n_segments, 128, 32), 128, 0, (cudaStream_t)stream>>>(
         *st, *cfg, *out, use_seg_min);
   return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
 }
