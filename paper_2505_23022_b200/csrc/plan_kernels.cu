@@ -1022,7 +1022,14 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
   if (ttft_guard) {
     const double d = wv ? fadd_(arr, tt0) : 0.0;  // core.py:50-53
     bool done = false;
-    if (__all_sync(SL_FULL, !wv || d >= 0.0)) {
+    if (SL_SORT32 && __all_sync(SL_FULL, !wv || d >= 0.0)) {
+      const int sr = warp_ldf_src32(d, wv, W, lane);
+      if (sr >= 0) {
+        src = sr;
+        done = true;
+      }
+    }
+    if (!SL_SORT32 && __all_sync(SL_FULL, !wv || d >= 0.0)) {
       uint64_t key = wv ? (((uint64_t)__double_as_longlong(d) & ~31ull) | (uint64_t)lane) : ~0ull;
 #pragma unroll
       for (int size = 2; size <= 32; size <<= 1) {
