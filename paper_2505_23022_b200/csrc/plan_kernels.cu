@@ -975,9 +975,100 @@ __device__ unsigned long long sl_fused_prof[16];
 #else
 #define SL_FSTAMP() do {} while (0)
 #endif
+// Warp pairs of the fused step (plan_fused_pair_kernel): the fold warp loads the
+// running set, computes its aggregates, sum(1/slo) and -- speculatively with the
+// pre-admission minimum -- the running part of vbs, hands them over through
+// shared memory (named barrier 1 + pair), then waits for the plan warp's final
+// minimum (barrier 5 + pair) and runs the credit phase on the entries it holds.
+struct PairShared {
+  long long lens;
+  double min_pre, inv, vf, vc;
+  int vn;
+  int has_min;
+  unsigned long long MIN;
+};
+__device__ __forceinline__ void pair_bar_sync(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ void pair_bar_arrive(int id) {
+  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
+}
+
+// The fold warp of a pair (see PairShared): running-set work of seg_plan_small.
+__device__ __forceinline__ void seg_plan_fold(const sl_plan_state& st, const sl_plan_config& cfg,
+                                              const sl_plan_out& out, int seg, int lane,
+                                              double* buf, PairShared& ps_sh, int pair) {
+  const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
+  if (cfg.flags & SL_PLAN_GUARD_ONLY) return;  // the plan warp stops after the walk
+  const int64_t rb = st.r_begin[seg];
+  const int R = (int)(st.r_begin[seg + 1] - rb);
+  const int E = st.credit_exp[seg];
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  const bool rv = lane < R;
+  double rt = 1.0;
+  int32_t rlen = 0;
+  uint64_t rcred = 0;
+  bool rex = false;
+  if (rv) {
+    rt = st.r_tpot[rb + lane];
+    rlen = st.r_cur_len[rb + lane];
+    rcred = st.r_credit[rb + lane];
+    rex = st.r_exclude && st.r_exclude[rb + lane];
+  }
+  // running aggregates (:117-124), sum(1/slo) (:121), vbs running part (:312-315)
+  const int64_t lens = warp_sum_i64(rv ? (int64_t)rlen : 0);
+  double min_pre = rv ? rt : kInf;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) min_pre = fmin(min_pre, __shfl_xor_sync(SL_FULL, min_pre, o));
+  double inv = 0.0;
+  if (tpot_guard && R > 0) {
+    PySum ps;
+    ps_init(ps);
+    ps_add_warp_smem(ps, frcp_(rt), R, buf);
+    inv = ps_result(ps);
+  }
+  PySum vs;
+  ps_init(vs);
+  if (R > 0) ps_add_warp_smem(vs, fdiv_(min_pre, rt), R, buf);
+  if (lane == 0) {
+    ps_sh.lens = lens;
+    ps_sh.min_pre = min_pre;
+    ps_sh.inv = inv;
+    ps_sh.vf = vs.f;
+    ps_sh.vc = vs.c;
+    ps_sh.vn = vs.n;
+  }
+  __syncwarp();
+  pair_bar_arrive(1 + pair);
+  pair_bar_sync(5 + pair);  // the plan warp's final minimum
+  const uint64_t MIN = ps_sh.MIN;
+  // ---- credit phase (:161-180) or decode-all
+  bool b = false;
+  uint64_t N = rcred;
+  if (rv && !rex) {
+    if (tpot_guard) {
+      const uint64_t S = slo_fixed<false>(rt, E);
+      N += MIN;
+      b = N >= S;
+      if (b) N -= S;
+    } else {
+      b = true;
+    }
+  }
+  const unsigned bm = __ballot_sync(SL_FULL, b);
+  if (rv) {
+    out.r_credit_out[rb + lane] = N;
+    out.r_batch[rb + lane] = b;
+    out.r_pos[rb + lane] = b ? __popc(bm & lanemask_lt()) : -1;
+  }
+  if (lane == 0) out.seg_counts[4 * seg + 3] = __popc(bm);
+}
+
+template <bool PAIR = false>
 __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl_plan_config& cfg,
                                                const sl_plan_out& out, int seg, int lane,
-                                               double* buf) {
+                                               double* buf, PairShared* ps_sh = nullptr,
+                                               int pair = 0) {
   const sl_cost& C = cfg.cost;
   const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -1010,7 +1101,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
   int32_t rlen = 0;
   uint64_t rcred = 0;
   bool rex = false;
-  if (rv) {
+  if (!PAIR && rv) {
     rt = st.r_tpot[rb + lane];
     rlen = st.r_cur_len[rb + lane];
     rcred = st.r_credit[rb + lane];
@@ -1140,15 +1231,28 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
   }
 
   // ---- running aggregates (:117-124)
-  int64_t lens = warp_sum_i64(rv ? (int64_t)rlen : 0);
-  double min_d = rv ? rt : kInf;
+  int64_t lens;
+  double min_d;
+  double inv_pair = 0.0;
+  if (PAIR) {  // from the fold warp
+    pair_bar_sync(1 + pair);
+    lens = ps_sh->lens;
+    min_d = ps_sh->min_pre;
+    inv_pair = ps_sh->inv;
+  } else {
+    lens = warp_sum_i64(rv ? (int64_t)rlen : 0);
+    min_d = rv ? rt : kInf;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) min_d = fmin(min_d, __shfl_xor_sync(SL_FULL, min_d, o));
+    for (int o = 16; o; o >>= 1) min_d = fmin(min_d, __shfl_xor_sync(SL_FULL, min_d, o));
+  }
+  const double min_pre = min_d;
   bool has_min = R > 0;
   unsigned admm = 0, keepm = 0, rejm = 0;
   if (tpot_guard) {
     double inv = 0.0;
-    if (kept && R > 0) {
+    if (PAIR) {
+      inv = inv_pair;
+    } else if (kept && R > 0) {
       PySum ps;
       ps_init(ps);
       ps_add_warp_smem(ps, frcp_(rt), R, buf);
@@ -1219,7 +1323,14 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
   if (has_min) {
     PySum vs;
     ps_init(vs);
-    if (R > 0) ps_add_warp_smem(vs, fdiv_(min_d, rt), R, buf);
+    if (PAIR && R > 0 && min_d == min_pre) {
+      vs.f = ps_sh->vf;  // the fold warp's running part, folded with this minimum
+      vs.c = ps_sh->vc;
+      vs.n = ps_sh->vn;
+    } else if (R > 0) {
+      if (PAIR && rv) rt = st.r_tpot[rb + lane];  // admission lowered the minimum (rare)
+      ps_add_warp_smem(vs, fdiv_(min_d, rt), R, buf);
+    }
     if (nadm) {
       const bool a = (admm >> lane) & 1u;
       const double x = a ? fdiv_(min_d, tp) : 0.0;
@@ -1232,6 +1343,11 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
   }
   SL_FSTAMP();
   const uint64_t MIN = has_min ? slo_fixed<false>(min_d, E) : ~0ull;
+  if (PAIR) {
+    if (lane == 0) ps_sh->MIN = MIN;
+    __syncwarp();
+    pair_bar_arrive(5 + pair);  // the fold warp runs the credit phase
+  }
   if (lane == 0) {
     out.seg_counts[4 * seg + 0] = __popc(keepm);
     out.seg_counts[4 * seg + 1] = nadm;
@@ -1240,6 +1356,7 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
     out.seg_min_slo[seg] = has_min ? min_d : __longlong_as_double(0x7ff8000000000000LL);
     out.seg_min_fixed[seg] = MIN;
   }
+  if (PAIR) return;
   // ---- credit phase (:161-180) or decode-all
   bool b = false;
   uint64_t N = rcred;
@@ -1261,6 +1378,37 @@ __device__ __forceinline__ void seg_plan_small(const sl_plan_state& st, const sl
   }
   if (lane == 0) out.seg_counts[4 * seg + 3] = __popc(bm);
   SL_FSTAMP();
+}
+
+// ---- the fused plan step with a warp pair per segment (PairShared): 4 segments
+// per 256-thread CTA; the plan warp sorts, walks and admits while the fold warp
+// reduces the running set; segments with more than 32 running run unpaired.
+__global__ void __launch_bounds__(256) plan_fused_pair_kernel(const sl_plan_state st,
+                                                              const sl_plan_config cfg,
+                                                              sl_plan_out out) {
+  __shared__ __align__(16) double bufs[8][32];
+  __shared__ PairShared psh[4];
+  const int w = threadIdx.x >> 5, pair = w >> 1;
+  const int seg = blockIdx.x * 4 + pair;
+  if (seg >= st.n_segments) return;
+  const int lane = threadIdx.x & 31;
+  const bool small = st.r_begin[seg + 1] - st.r_begin[seg] <= 32;  // (w <= 32 here)
+  if (small) {
+    if (w & 1)
+      seg_plan_fold(st, cfg, out, seg, lane, bufs[w], psh[pair], pair);
+    else
+      seg_plan_small<true>(st, cfg, out, seg, lane, bufs[w], &psh[pair], pair);
+    return;
+  }
+  if (w & 1) return;
+  if (cfg.flags & SL_FLAG_TTFT_GUARD) {
+    seg_sort_warp(st, out.perm, seg, lane);
+    __syncwarp();
+  }
+  seg_guard_admit(st, cfg, out, seg, lane);
+  if (cfg.flags & SL_PLAN_GUARD_ONLY) return;
+  __syncwarp();
+  seg_credit_select(st, cfg, out, 1, seg, lane);
 }
 
 // ---- the whole plan_step in one launch (segments of <= 32 waiting items):
@@ -1513,6 +1661,12 @@ int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64
          !out->r_credit_out || !out->r_batch || !out->r_pos))
       return SL_ERR_ARG;
     if (st->n_segments == 0) return SL_OK;
+    const char* pe = getenv("SL_PLAN_PAIR");  // warp pairs (default) or one warp per segment
+    if (!(pe && pe[0] == '0')) {
+      plan_fused_pair_kernel<<<(st->n_segments + 3) / 4, 256, 0, (cudaStream_t)stream>>>(*st, *cfg,
+                                                                                       *out);
+      return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
+    }
     plan_fused_kernel<<<warps_grid(st->n_segments, 256), 256, 0, (cudaStream_t)stream>>>(*st, *cfg,
                                                                                         *out);
     return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
