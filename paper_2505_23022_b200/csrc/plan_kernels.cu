@@ -1661,8 +1661,11 @@ int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64
          !out->r_credit_out || !out->r_batch || !out->r_pos))
       return SL_ERR_ARG;
     if (st->n_segments == 0) return SL_OK;
-    const char* pe = getenv("SL_PLAN_PAIR");  // warp pairs (default) or one warp per segment
-    if (!(pe && pe[0] == '0')) {
+    // warp pairs while the GPU has room for them (measured: faster up to ~1,500
+    // segments, one warp per segment from 2,048); SL_PLAN_PAIR=0 / =1 forces
+    const char* pe = getenv("SL_PLAN_PAIR");
+    const bool pair = pe ? pe[0] != '0' : st->n_segments <= 1536;
+    if (pair) {
       plan_fused_pair_kernel<<<(st->n_segments + 3) / 4, 256, 0, (cudaStream_t)stream>>>(*st, *cfg,
                                                                                        *out);
       return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
