@@ -83,6 +83,24 @@ __device__ unsigned long long sl_prof_cycles[kProfSims][kProfSlots];
   prof_acc[15] = prof_gtime();                                             \
   if (lane == 0 && (si) < kProfSims)                                       \
     for (int k_ = 0; k_ < kProfSlots; ++k_) sl_prof_cycles[si][k_] = prof_acc[k_];
+#elif defined(SL_TIMELINE)
+// Timeline-only build (-DSL_TIMELINE): %globaltimer at each sim's start and end,
+// stored straight to global memory (no live registers), read with
+// sl_phase_prof_read into slots 14-15.
+constexpr int kProfSims = 1 << 16;
+constexpr int kProfSlots = 26;
+__device__ unsigned long long sl_prof_cycles[kProfSims][kProfSlots];
+__device__ __forceinline__ unsigned long long prof_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SL_PROF_DECL \
+  if (lane == 0 && si < kProfSims) sl_prof_cycles[si][14] = prof_gtime();
+#define SL_PROF_MARK(k)
+#define SL_PROF_COUNT(k, v)
+#define SL_PROF_WRITE(si) \
+  if (lane == 0 && (si) < kProfSims) sl_prof_cycles[si][15] = prof_gtime();
 #else
 #define SL_PROF_DECL
 #define SL_PROF_MARK(k)
@@ -648,6 +666,10 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
   bool have = false;
   bool ret = false;
 #if SL_QUIET_PIPE
+#if SL_QUIET_SMEM
+  uint4* ring = reinterpret_cast<uint4*>(scr);
+  int flushed = 0;  // steps [0, flushed) of this call are hashed
+#endif
   // One-step software pipeline: the credit recurrence does not depend on the
   // clock, so step k+1's batch (credits, ballot, length / hash sums) is formed
   // while step k's itl() chain is in flight, and committed only when step k+1
@@ -673,23 +695,49 @@ __device__ __forceinline__ bool quiet_steps(const Sim& s, const KArgs& a, bool h
       blen1 = __reduce_add_sync(SL_FULL, b1 ? (unsigned)sl[0].cur_len : 0u);
       bh1 = __reduce_add_sync(SL_FULL, b1 ? hh : 0u);
       const double end = fadd_(now, itl(C, nb, div_small((double)blen, nb)));
+#if SL_QUIET_SMEM
+      if (lane == (k & 31)) {
+        const uint64_t eb = (uint64_t)__double_as_longlong(end);
+        ring[k & 31] = make_uint4((unsigned)nb, bh, (unsigned)eb, (unsigned)(eb >> 32));
+      }
+#else
       if (lane == (k & 31)) {
         end_bits = (uint64_t)__double_as_longlong(end);
         d_nb = nb;
         d_bh = bh;
         have = true;
       }
+#endif
       now = end;
       ++k;
       if (ret || !(now < lim)) break;
       if ((k & 31) == 0) {
+#if SL_QUIET_SMEM
+        __syncwarp();
+        const uint4 q = ring[lane];
+        const uint64_t st = (uint64_t)(step0 + k - 32 + lane);
+        acc.dig += digest_item(st, 2, q.x, q.y) +
+                   digest_item(st, 3, 0, ((uint64_t)q.w << 32) | q.z);
+        flushed = k;
+        __syncwarp();
+#else
         if (have)
           acc.dig += digest_item((uint64_t)(step0 + k - 32 + lane), 2, d_nb, d_bh) +
                      digest_item((uint64_t)(step0 + k - 32 + lane), 3, 0, end_bits);
         have = false;
+#endif
       }
     }
   }
+#if SL_QUIET_SMEM
+  __syncwarp();
+  if (flushed + lane < k) {
+    const uint4 q = ring[lane];
+    const uint64_t st = (uint64_t)(step0 + flushed + lane);
+    acc.dig += digest_item(st, 2, q.x, q.y) + digest_item(st, 3, 0, ((uint64_t)q.w << 32) | q.z);
+  }
+  __syncwarp();
+#endif
 #elif SL_QUIET_SMEM
   // the step's digest inputs (batch size, batch hash, end time) go to a 32-entry
   // ring in the (here unused) scratch: one lane's store per step, hashed 32 steps

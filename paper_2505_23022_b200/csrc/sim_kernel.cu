@@ -813,7 +813,7 @@ int sl_selftest_div_small(const double* a, const int32_t* b, double* out, int64_
 
 int sl_run_batch_launches(void) { return 4; }  // WRec pre-pass + hot fast + generic fast + handoff
 
-#ifdef SL_PHASE_PROF
+#if defined(SL_PHASE_PROF) || defined(SL_TIMELINE)
 // Profiling builds only: per-sim phase cycles / counts of the fast kernel.
 int sl_phase_prof_read(uint64_t* out, int32_t n_sims) {
   if (n_sims > kProfSims) n_sims = kProfSims;
