@@ -289,7 +289,8 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
                                                 double inv_pre = 0.0, double* min_out = nullptr,
                                                 bool* has_min_out = nullptr,
                                                 int* nadm_out = nullptr,
-                                                int32_t* klist32 = nullptr) {
+                                                int32_t* klist32 = nullptr,
+                                                long long lens_pre = 0, double min_pre = 0.0) {
   const sl_cost& C = cfg.cost;
   const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -436,17 +437,22 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
     return;
   }
 
-  // 2. running aggregates (sched_scorpio.py:117-124)
-  int64_t lens = 0;
-  double min_d = __longlong_as_double(0x7ff0000000000000LL);
+  // 2. running aggregates (sched_scorpio.py:117-124); GROUP: reduced lane-per-
+  // segment by the caller with its sum(1/slo) fold
+  int64_t lens = lens_pre;
+  double min_d = min_pre;
+  if (!GROUP) {
+    lens = 0;
+    min_d = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll 4
-  for (int j = lane; j < R; j += 32) {
-    lens += st.r_cur_len[rb + j];
-    min_d = fmin(min_d, st.r_tpot[rb + j]);
-  }
-  lens = warp_sum_i64(lens);
+    for (int j = lane; j < R; j += 32) {
+      lens += st.r_cur_len[rb + j];
+      min_d = fmin(min_d, st.r_tpot[rb + j]);
+    }
+    lens = warp_sum_i64(lens);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) min_d = fmin(min_d, __shfl_xor_sync(SL_FULL, min_d, o));
+    for (int o = 16; o; o >>= 1) min_d = fmin(min_d, __shfl_xor_sync(SL_FULL, min_d, o));
+  }
   bool has_min = R > 0;
   int nadm = 0, nwait = 0;
   int32_t* adm = out.adm_order + wb;
@@ -622,13 +628,20 @@ __global__ void __launch_bounds__(128, SL_PLAN_GROUP_BLOCKS) guard_admit_group_k
   const int my = seg0 + lane;
   const bool mine = lane < nseg;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
-  // fold 1: sum(1.0 / slo) over this lane's segment's running entries, in order
-  double inv = 0.0;
-  if (mine && tpot_guard) {
+  // fold 1: sum(1.0 / slo) over this lane's segment's running entries, in order,
+  // with the segment's min slo and sum of current lengths
+  double inv = 0.0, mn = __longlong_as_double(0x7ff0000000000000LL);
+  long long lsum = 0;
+  if (mine) {
     const int64_t rb = st.r_begin[my], re = st.r_begin[my + 1];
     PySum ps;
     ps_init(ps);
-    for (int64_t j = rb; j < re; ++j) ps_add(ps, frcp_(st.r_tpot[j]));
+    for (int64_t j = rb; j < re; ++j) {
+      const double t = st.r_tpot[j];
+      if (tpot_guard) ps_add(ps, frcp_(t));
+      mn = fmin(mn, t);
+      lsum += st.r_cur_len[j];
+    }
     inv = ps_result(ps);
   }
   double min_d = 0.0;
@@ -639,7 +652,8 @@ __global__ void __launch_bounds__(128, SL_PLAN_GROUP_BLOCKS) guard_admit_group_k
     bool h_k = false;
     int a_k = 0;
     seg_guard_admit<true>(st, cfg, out, seg0 + k, lane, __shfl_sync(SL_FULL, inv, k), &m_k, &h_k,
-                          &a_k, klist[threadIdx.x >> 5]);
+                          &a_k, klist[threadIdx.x >> 5], __shfl_sync(SL_FULL, lsum, k),
+                          __shfl_sync(SL_FULL, mn, k));
     __syncwarp();  // the next segment reuses the warp's kept-list buffer
     if (lane == k) {
       min_d = m_k;
