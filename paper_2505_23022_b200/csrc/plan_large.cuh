@@ -120,20 +120,41 @@ struct LargeSmem {
   long long lens;  // sum of current lengths over running
   double red_min[2];
   long long red_len[2];
-  int agg_ready, inv_ready, vbs_ready;  // split launch: set by the fold CTA, polled by warp 0
+  // split launch: one-shot mbarriers (expected count 1) in CTA 0, arrived on by
+  // the fold CTA after it has stored its results there, waited on by warp 0
+  unsigned long long agg_ready, inv_ready, vbs_ready;
 };
 
 // Split launch (a cluster of 2 CTAs per segment): the fold warps run in CTA 1 on
-// their own SM and publish their results into CTA 0's shared memory, then set a
-// ready flag there (release at cluster scope); warp 0 of CTA 0 polls the flag
-// (acquire) where it would otherwise wait on the named barrier.
-__device__ __forceinline__ void flag_release(int* remote_flag) {
-  __threadfence();  // the results (DSMEM stores) before the flag
-  *reinterpret_cast<volatile int*>(remote_flag) = 1;
+// their own SM and publish their results into CTA 0's shared memory, then
+// arrive (release, cluster scope) on an mbarrier there; warp 0 of CTA 0 waits
+// on it (acquire) where it would otherwise wait on the named barrier.
+__device__ __forceinline__ void mbar_init1(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
 }
-__device__ __forceinline__ void flag_acquire(const int* local_flag) {
-  while (*reinterpret_cast<const volatile int*>(local_flag) == 0) __nanosleep(64);
-  __threadfence();  // the flag before the results
+__device__ __forceinline__ void flag_release(unsigned long long* local_bar_in_cta0) {
+  // the mbarrier at the same offset in CTA 0's shared memory
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;"
+               : "=r"(remote)
+               : "r"((unsigned)__cvta_generic_to_shared(local_bar_in_cta0)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+__device__ __forceinline__ void flag_acquire(unsigned long long* bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a)
+        : "memory");
+  }
 }
 
 // exclusive scan of the kLChunks counts of row r (warp 0), totals to *tot
@@ -320,11 +341,12 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   if (tid == 0 && crank == 0) SL_LSTAMP(7);  // kernel entry
   if (split) {
     if (tid == 0) {
-      sm.agg_ready = 0;
-      sm.inv_ready = 0;
-      sm.vbs_ready = 0;
+      mbar_init1(&sm.agg_ready);
+      mbar_init1(&sm.inv_ready);
+      mbar_init1(&sm.vbs_ready);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    cl.sync();  // both CTAs started, flags cleared, before any DSMEM store
+    cl.sync();  // both CTAs started, mbarriers initialised, before any DSMEM access
   }
   LargeSmem* res = split ? cl.map_shared_rank(&sm, 0) : &sm;  // where fold results go
   const sl_cost& C = cfg.cost;
@@ -392,7 +414,7 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       if (f == 1) SL_LSTAMP(2);
       if (split) {  // the inv pair alone: the min / lengths warps do not wait for it
         bar_sync(kBarInvPair, 64);
-        if (f == 1 && lane == 0) flag_release(&res->inv_ready);
+        if (f == 1 && lane == 0) flag_release(&sm.inv_ready);
       } else {
         bar_arrive(kBarAgg, agg_cnt);
       }
@@ -421,7 +443,7 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     }
     if (f == 3) SL_LSTAMP(3);
     if (split) {
-      if (f == 3 && lane == 0) flag_release(&res->agg_ready);  // min / lengths
+      if (f == 3 && lane == 0) flag_release(&sm.agg_ready);  // min / lengths
     } else {
       bar_arrive(kBarAgg, agg_cnt);
     }
@@ -437,7 +459,7 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       }
       if (split) {
         bar_sync(kBarVbs, vbs_cnt);
-        if (f == 3 && lane == 0) flag_release(&res->vbs_ready);
+        if (f == 3 && lane == 0) flag_release(&sm.vbs_ready);
       } else {
         bar_arrive(kBarVbs, vbs_cnt);  // warp 0 waits on it iff R > 0
       }
