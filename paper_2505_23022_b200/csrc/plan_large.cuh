@@ -207,16 +207,20 @@ __device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double pr
     // first one that passes at the current prefix
     bool a0 = v0, a1 = v1, k0 = false, k1 = false;
     for (;;) {
+      // every lane also forms the prefix it would leave if kept (prefix + its
+      // prefill, the same IEEE add) alongside the tests, so that the next
+      // prefix is one shuffle away from the first passing lane
+      const double n0 = fadd_(prefix, p0), n1 = fadd_(prefix, p1);
       const unsigned ok0 = __ballot_sync(SL_FULL, a0 && !(fadd_(fadd_(e0, prefix), p0) > t0));
       const unsigned ok1 = __ballot_sync(SL_FULL, a1 && !(fadd_(fadd_(e1, prefix), p1) > t1));
       if (!(ok0 | ok1)) break;  // every remaining item fails at this prefix
       const int g = ok0 ? __ffs(ok0) - 1 : 32 + __ffs(ok1) - 1;
-      const double pg = g < 32 ? bcast(p0, g) : bcast(p1, g - 32);
+      const double q0 = __shfl_sync(SL_FULL, n0, g & 31), q1 = __shfl_sync(SL_FULL, n1, g & 31);
       k0 |= lane == g;
       k1 |= lane + 32 == g;
       a0 &= lane > g;
       a1 &= lane + 32 > g;
-      prefix = fadd_(prefix, pg);
+      prefix = g < 32 ? q0 : q1;
     }
     if (v0) sm.dec[j0] = !k0;
     if (v1) sm.dec[j1] = !k1;
