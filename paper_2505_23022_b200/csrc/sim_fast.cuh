@@ -244,6 +244,160 @@ __device__ __forceinline__ bool cert_scan(const Sim& s, double now, int W, int c
   return all_ok;
 }
 
+#ifndef SL_BOUND_WALK
+#define SL_BOUND_WALK 1  // two-sided certified walk (see spec_walk_bounds)
+#endif
+#ifndef SL_WALK_MARGIN
+// relative margin of the walk's prefix bounds (2^-30); any larger value is as
+// exact (wider bounds, more chunks on the serial form): the parity tests run a
+// 2^-8 build to exercise that form (tests/test_gpu_walk_forms.py)
+#define SL_WALK_MARGIN 9.313225746154785e-10
+#endif
+
+// Rejection side effects of one walk chunk and the stable compaction of its
+// kept items to wl[kept, ...) (shared by both walk forms).
+__device__ __forceinline__ void walk_commit(const Sim& s, const KArgs& a, bool has_out, int& kept,
+                                            int& nrej, bool valid, int idx, unsigned rejm,
+                                            int64_t step, Acc& acc, int lane, int64_t lg_rej,
+                                            int64_t cap_rej) {
+  const bool r_ = valid && ((rejm >> lane) & 1u);
+  const bool keep = valid && !r_;
+  const unsigned km = __ballot_sync(SL_FULL, keep);
+  __syncwarp();
+  if (keep) s.wl[kept + __popc(km & lanemask_lt())] = idx;
+  if (r_) {
+    const int pos = nrej + __popc(rejm & lanemask_lt());
+    const int64_t rid = s.id[idx];
+    acc.dig_rej += digest_item((uint64_t)step, 1, (uint32_t)pos, (uint64_t)rid * 2u);
+    SL_ACC_ADD(acc, rej_ttft, kAccRejTtft, 1);
+    if (has_out) a.out.status[s.out_off + idx] = SL_REJECTED_TTFT;
+    if (lg_rej >= 0 && pos < cap_rej) a.log.rej_ids[lg_rej + pos] = rid * 2;
+  }
+  __syncwarp();
+  kept += __popc(km);
+  nrej += __popc(rejm);
+}
+
+// TTFT prefix walk, two-sided certified form (ttft_guard sched_scorpio.py:196-205;
+// early_reject sched_baselines.py:95-103).  The exact walk keeps a sequential
+// fl-sum `prefix` of the kept prefills and rejects item j iff
+// fl(fl(e_j + prefix_j) + pf_j) > ttft_j, e_j = fl(now - arr_j).  That test is
+// monotone in prefix_j, so bounds Lj <= prefix_j <= Uj decide it exactly
+// whenever both agree.  Per chunk, one warp scan (any order) of the prefills of
+// the items not yet rejected gives excl_j; with Pl <= (exact real sum of the
+// kept prefills before the chunk) <= ... and Pu an upper bound of the
+// sequential prefix,
+//   Uj = fl(fl(Pu + excl_j) (1 + 2^-30)),  Lj = fl(fl(Pl + excl_j) (1 - 2^-30))
+// bound prefix_j: any-order fl-sums of n < 2^20 non-negative terms are within
+// (n-1) u < 2^-33 relative of the real sum, which the 2^-30 factors dominate
+// (with the rounding of the two ops).  The first item that is not certain to
+// pass is either certain to fail (rejected; the chunk is re-scanned without it,
+// since later prefixes shrink) or undecided (|est - ttft| within ~2^-29 of the
+// prefix): then the chunk runs the serial exact walk from the exact prefix (the
+// sequential sum of the kept prefills so far, recomputed when not known).
+// Items failing at Pl fail at any prefix: rejected outright.  Returns true when
+// anything was rejected or a chunk ran serially; `until` / `p_up` as spec_walk.
+__device__ __forceinline__ bool spec_walk_bounds(const Sim& s, const KArgs& a, bool has_out,
+                                                 int& W, int& nrej, double now, int64_t step,
+                                                 Acc& acc, int lane, int64_t lg_rej,
+                                                 int64_t cap_rej, double* bc, double& until,
+                                                 double& p_up) {
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  const double up = 1.0 + SL_WALK_MARGIN, dn = 1.0 - SL_WALK_MARGIN;
+  const bool certifiable = W < (1 << 20);
+  double Pl = 0.0, Pu = 0.0;  // bounds of the incoming prefix (equal and exact while pex)
+  bool pex = true;
+  double tmin = kInf;
+  int kept = 0;
+  bool any = false;
+  for (int c0 = 0; c0 < W; c0 += 32) {
+    const int j = c0 + lane;
+    const bool valid = j < W;
+    int idx = 0;
+    double e = 0.0, pf = 0.0, tt = 0.0;
+    if (valid) {
+      idx = s.wl[j];
+      const WRec& r = s.wr[idx];
+      e = fsub_(now, r.arr);
+      pf = r.prefill;
+      tt = r.ttft;
+    }
+    unsigned rejm = __ballot_sync(SL_FULL, valid && fadd_(fadd_(e, Pl), pf) > tt);
+    bool serial = !certifiable;
+    double Uj = 0.0, estU = 0.0, tot = 0.0;
+    while (!serial) {
+      const bool live = valid && !((rejm >> lane) & 1u);
+      double v = live ? pf : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(SL_FULL, v, o);
+        if (lane >= o) v = fadd_(v, y);
+      }
+      double excl = __shfl_up_sync(SL_FULL, v, 1);
+      if (lane == 0) excl = 0.0;
+      tot = __shfl_sync(SL_FULL, v, 31);
+      Uj = fmul_(fadd_(Pu, excl), up);
+      estU = fadd_(fadd_(e, Uj), pf);
+      const unsigned m = __ballot_sync(SL_FULL, live && !(estU <= tt));
+      if (!m) break;
+      const int f = __ffs(m) - 1;
+      const double Lj = fmul_(fadd_(Pl, excl), dn);
+      const bool fails = fadd_(fadd_(e, Lj), pf) > tt;
+      if (__shfl_sync(SL_FULL, (int)fails, f)) {
+        rejm |= 1u << f;
+      } else {
+        serial = true;
+      }
+    }
+    if (!serial) {
+      if (valid && !((rejm >> lane) & 1u))
+        tmin = fmin(tmin, walk_pass_until(now, Uj, pf, tt, estU));
+      Pl = fmul_(fadd_(Pl, tot), dn);
+      Pu = fmul_(fadd_(Pu, tot), up);
+      pex = false;
+    } else {
+      // exact incoming prefix, then the reference's loop over the chunk
+      double p = Pl;
+      if (!pex) {
+        p = 0.0;
+        for (int t = 0; t < kept; ++t) p = fadd_(p, s.wr[s.wl[t]].prefill);
+      }
+      double* bcE = bc + 32;
+      double* bcT = bc + 64;
+      bc[lane] = pf;
+      bcE[lane] = e;
+      bcT[lane] = tt;
+      __syncwarp();
+      rejm = 0u;
+      double mine = 0.0;
+      const int cnt = min(32, W - c0);
+      for (int t = 0; t < cnt; ++t) {
+        const double pt = bc[t];
+        if (lane == t) mine = p;
+        if (fadd_(fadd_(bcE[t], p), pt) > bcT[t])
+          rejm |= 1u << t;
+        else
+          p = fadd_(p, pt);
+      }
+      __syncwarp();
+      if (valid && !((rejm >> lane) & 1u))
+        tmin = fmin(tmin, walk_pass_until(now, mine, pf, tt, fadd_(fadd_(e, mine), pf)));
+      Pl = Pu = p;
+      pex = true;
+      any = true;
+    }
+    if (rejm) any = true;
+    if (rejm || kept != c0)
+      walk_commit(s, a, has_out, kept, nrej, valid, idx, rejm, step, acc, lane, lg_rej, cap_rej);
+    else
+      kept += min(32, W - c0);
+  }
+  W = kept;
+  until = warp_min_nonneg(tmin);
+  p_up = pex ? fmul_(Pu, up) : Pu;
+  return any;
+}
+
 // TTFT prefix walk over wl[0, W) in list order (ttft_guard sched_scorpio.py:196-205;
 // early_reject sched_baselines.py:95-103).
 //  1. Certified pass: an upper bound U_j of the sequential prefix (warp scan in
@@ -260,6 +414,10 @@ __device__ __forceinline__ bool spec_walk(const Sim& s, const KArgs& a, bool has
                                           int& nrej, double now, int64_t step, Acc& acc, int lane,
                                           int64_t lg_rej, int64_t cap_rej, double* bc,
                                           double& until, double& p_up) {
+#if SL_BOUND_WALK
+  return spec_walk_bounds(s, a, has_out, W, nrej, now, step, acc, lane, lg_rej, cap_rej, bc,
+                          until, p_up);
+#endif
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   const bool certifiable = W < (1 << 20);
   if (certifiable) {
