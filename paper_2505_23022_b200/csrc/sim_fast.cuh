@@ -244,6 +244,9 @@ __device__ __forceinline__ bool cert_scan(const Sim& s, double now, int W, int c
   return all_ok;
 }
 
+#ifndef SL_BLOCK_ARR
+#define SL_BLOCK_ARR 1  // a blocked queue stays blocked across a failing arrival
+#endif
 #ifndef SL_BOUND_WALK
 #define SL_BOUND_WALK 1  // two-sided certified walk (see spec_walk_bounds)
 #endif
@@ -1136,8 +1139,28 @@ __device__ __forceinline__ void run_fast(Sim& s, const KArgs& a, bool has_out, i
 #else
       process_arrivals<WIDE>(s, W, next, next_t, now, sorted_ldf, sjf, lane);
 #endif
+      const bool was_blocked = blocked;
       arrivals_keep_bounds(s, n0, (int)(next - n0), now, ttft_guard, blocked, walk_until, p_up,
                            lane);
+#if SL_BLOCK_ARR
+      // A blocked queue (every waiting request fails against the unchanged
+      // running state and is feasible alone) stays blocked when the one new
+      // request fails against that state too and is feasible alone: this
+      // step's scan would admit and reject nothing.
+      if (HOT && was_blocked && mono && next - n0 == 1) {
+        const WRec& w = s.wr[n0];
+        const double tp = w.tpot, ic = w.inv;
+        const int32_t ps_ = w.pred_solo;
+        const bool has_min = R > 0;
+        const bool lt = !has_min || tp < g.min_d;
+        const double minp = lt ? tp : g.min_d;
+        const double V = fmul_(minp, fadd_(ps_result(g.pinv), ic));
+        const double L = div_small((double)(g.lens + w.prompt), R + 1);
+        const double est = tpot_estimate(C, V, L, ps_ & 0x7fffffff);
+        const double thr = (r_only && has_min) ? g.min_d : minp;
+        blocked = !(est <= thr) && (ps_ & (int32_t)0x80000000) != 0;
+      }
+#endif
     }
     SL_PROF_MARK(0)
     if (has_h && now >= s.horizon) break;  // simengine.py:190-191
