@@ -492,7 +492,9 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
         const bool lt = !has_min || tp < min_d;
         const double minp = lt ? tp : min_d;
         const double V = fmul_(minp, fadd_(inv, ic));
-        const double L = fdiv_((double)(lens + ln), (double)(n_run + 1));
+        // Python's int / int: exact small-divisor form up to 128 (div_small)
+        const double L = n_run < 128 ? div_small((double)(lens + ln), (int)(n_run + 1))
+                                     : fdiv_((double)(lens + ln), (double)(n_run + 1));
         const double est = tpot_estimate(C, V, L, pred);
         const double thr = (r_only && has_min) ? min_d : minp;
         const bool ok = ((pend >> lane) & 1u) && est <= thr;
