@@ -279,6 +279,24 @@ __global__ void copy_kernel(const sl_plan_state st, const int32_t* __restrict__ 
     dst[i] = src[i];
 }
 
+// A segment's waiting-item fields staged in shared memory by cp.async while the
+// warp works on the previous segment (guard_admit_group_kernel, <= 32 waiting).
+struct GStage {
+  double arr[32], pf[32], tt[32], tp[32];
+  int32_t idx[32], ln[32], pd[32], klane[32];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 // ---- guard + admission: one warp per segment
 // GROUP: the Neumaier folds are done lane-per-segment by the caller
 // (guard_admit_group_kernel): `inv_pre` is this segment's sum(1/slo) fold, and
@@ -290,7 +308,8 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
                                                 bool* has_min_out = nullptr,
                                                 int* nadm_out = nullptr,
                                                 int32_t* klist32 = nullptr,
-                                                long long lens_pre = 0, double min_pre = 0.0) {
+                                                long long lens_pre = 0, double min_pre = 0.0,
+                                                GStage* stg = nullptr) {
   const sl_cost& C = cfg.cost;
   const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
   const bool tpot_guard = cfg.flags & SL_FLAG_TPOT_GUARD;
@@ -310,6 +329,8 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
   // waiting (no global round trip), else the segment's slice of out.scratch
   int32_t* kept_list = (klist32 && W <= 32) ? klist32 : out.scratch + wb;
   int nrej = 0, kept = 0;
+  // fields staged in shared memory by the caller (one chunk: lane == position)
+  const bool staged = stg != nullptr && W <= 32;
 
   // 1. TTFT walk over the LDF order (speculative-parallel, exact), or the FCFS queue.
   // Certified pass first (as spec_walk in sim_fast.cuh): an inflated any-order
@@ -325,7 +346,11 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
       const int p = c0 + lane;
       const bool valid = p < W;
       double e = 0.0, pf = 0.0, tt = 0.0;
-      if (valid) {
+      if (valid && staged) {
+        e = fsub_(now, stg->arr[lane]);
+        pf = stg->pf[lane];
+        tt = stg->tt[lane];
+      } else if (valid) {
         const int32_t idx = ttft_guard ? out.perm[wb + p] : (int32_t)(wb + p);
         e = fsub_(now, st.w_arrival[idx]);
         pf = st.w_prefill[idx];
@@ -354,9 +379,16 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
       const int p = c0 + lane;
       return p < W ? (ttft_guard ? out.perm[wb + p] : (int32_t)(wb + p)) : -1;
     };
-    int32_t idx_n = slot(0), idx_nn = slot(32);
+    int32_t idx_n = staged ? (lane < W ? stg->idx[lane] : -1) : slot(0);
+    int32_t idx_nn = staged ? -1 : slot(32);
     double ar_n = 0.0, pf_n = 0.0, tt_n = 0.0;
-    if (idx_n >= 0) {
+    if (staged) {
+      if (idx_n >= 0) {
+        ar_n = stg->arr[lane];
+        pf_n = stg->pf[lane];
+        tt_n = stg->tt[lane];
+      }
+    } else if (idx_n >= 0) {
       ar_n = st.w_arrival[idx_n];
       pf_n = st.w_prefill[idx_n];
       tt_n = st.w_ttft[idx_n];
@@ -414,7 +446,11 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
       const bool rj = valid && ((rejm >> lane) & 1u);
       const bool keep = valid && !rj;
       const unsigned km = __ballot_sync(SL_FULL, keep);
-      if (keep) kept_list[kept + __popc(km & lanemask_lt())] = idx;
+      if (keep) {
+        const int q = kept + __popc(km & lanemask_lt());
+        kept_list[q] = idx;
+        if (staged) stg->klane[q] = lane;
+      }
       if (rj) {
         out.w_status[idx] = SL_PLAN_REJECTED_TTFT;
         out.w_pos[idx] = nrej + __popc(rejm & lanemask_lt());
@@ -480,10 +516,17 @@ __device__ __forceinline__ void seg_guard_admit(const sl_plan_state& st, const s
       double tp = 1.0, ic = 0.0;
       if (valid) {
         idx = kept_list[p];
-        tp = st.w_tpot[idx];
+        if (staged) {
+          const int q = stg->klane[p];
+          tp = stg->tp[q];
+          ln = stg->ln[q];
+          pred = stg->pd[q];
+        } else {
+          tp = st.w_tpot[idx];
+          ln = st.w_prompt[idx];
+          pred = st.w_pred[idx];
+        }
         ic = frcp_(tp);
-        ln = st.w_prompt[idx];
-        pred = st.w_pred[idx];
       }
       // feasible alone? (solo test, :279-289)
       const bool solo = solo_ok(C, tp, ic, ln, pred);
@@ -615,6 +658,9 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
 #ifndef SL_PLAN_GROUP
 #define SL_PLAN_GROUP 16  // segments per warp (measured: 16 with 7 blocks/SM beats 32, 8 and 4)
 #endif
+#ifndef SL_PLAN_STAGE
+#define SL_PLAN_STAGE 1  // cp.async staging of the next segment's fields (group kernel)
+#endif
 #ifndef SL_PLAN_GROUP_BLOCKS
 #define SL_PLAN_GROUP_BLOCKS 7  // <= 72 registers: 28 warps/SM
 #endif
@@ -649,14 +695,51 @@ __global__ void __launch_bounds__(128, SL_PLAN_GROUP_BLOCKS) guard_admit_group_k
   double min_d = 0.0;
   bool has_min = false;
   int nadm = 0;
+#if SL_PLAN_STAGE
+  // segment k+1's waiting fields are copied into shared memory (cp.async)
+  // while the warp walks and admits segment k; segment k+2's queue slots are
+  // loaded into a register meanwhile (two dependent global round trips per
+  // segment off the warp's path)
+  __shared__ GStage stage[4][2];
+  GStage* sg = stage[threadIdx.x >> 5];
+  const bool ttft_guard = cfg.flags & SL_FLAG_TTFT_GUARD;
+  auto seg_slot = [&](int seg) -> int32_t {
+    const int64_t wb = st.w_begin[seg];
+    const int W = (int)(st.w_begin[seg + 1] - wb);
+    return (W <= 32 && lane < W) ? (ttft_guard ? out.perm[wb + lane] : (int32_t)(wb + lane)) : -1;
+  };
+  auto issue = [&](GStage& b, int32_t idx) {
+    b.idx[lane] = idx;
+    if (idx >= 0) {
+      cp_async8(&b.arr[lane], st.w_arrival + idx);
+      cp_async8(&b.pf[lane], st.w_prefill + idx);
+      cp_async8(&b.tt[lane], st.w_ttft + idx);
+      cp_async8(&b.tp[lane], st.w_tpot + idx);
+      cp_async4(&b.ln[lane], st.w_prompt + idx);
+      cp_async4(&b.pd[lane], st.w_pred + idx);
+    }
+    cp_async_commit();
+  };
+  issue(sg[0], seg_slot(seg0));
+  int32_t i_next = nseg > 1 ? seg_slot(seg0 + 1) : -1;
+#endif
   for (int k = 0; k < nseg; ++k) {
     double m_k = 0.0;
     bool h_k = false;
     int a_k = 0;
+#if SL_PLAN_STAGE
+    issue(sg[(k + 1) & 1], i_next);  // (an empty group past the last segment)
+    i_next = k + 2 < nseg ? seg_slot(seg0 + k + 2) : -1;
+    cp_async_wait1();  // segment k's group has landed
+    __syncwarp();
+    GStage* cur = &sg[k & 1];
+#else
+    GStage* cur = nullptr;
+#endif
     seg_guard_admit<true>(st, cfg, out, seg0 + k, lane, __shfl_sync(SL_FULL, inv, k), &m_k, &h_k,
                           &a_k, klist[threadIdx.x >> 5], __shfl_sync(SL_FULL, lsum, k),
-                          __shfl_sync(SL_FULL, mn, k));
-    __syncwarp();  // the next segment reuses the warp's kept-list buffer
+                          __shfl_sync(SL_FULL, mn, k), cur);
+    __syncwarp();  // the next segment reuses the warp's kept-list and stage buffers
     if (lane == k) {
       min_d = m_k;
       has_min = h_k;
