@@ -28,14 +28,19 @@ def config2_arrays(n_segments: int, w: int, r: int, seed: int, now: float = 10.0
     that deadlines tie exactly, between equal arrivals (then the id decides)
     and between different ones (a1 + t1 == a2 + t2)."""
     rng = np.random.default_rng(seed)
-    S, W, R = n_segments, n_segments * w, n_segments * r
+    S = n_segments
+    # w / r: per-segment counts (ragged batches) or one count for every segment
+    ws = np.full(S, w, np.int64) if np.isscalar(w) else np.asarray(w, np.int64)
+    rs = np.full(S, r, np.int64) if np.isscalar(r) else np.asarray(r, np.int64)
+    assert len(ws) == S and len(rs) == S
+    W, R = int(ws.sum()), int(rs.sum())
     tier_w = rng.integers(0, 3, W)
     tier_r = rng.integers(0, 3, R)
     out_w = rng.integers(5, 401, W)
     out_r = rng.integers(5, 401, R)
     a = {
-        "w_begin": np.arange(S + 1, dtype=np.int64) * w,
-        "r_begin": np.arange(S + 1, dtype=np.int64) * r,
+        "w_begin": np.concatenate([[0], np.cumsum(ws)]).astype(np.int64),
+        "r_begin": np.concatenate([[0], np.cumsum(rs)]).astype(np.int64),
         "w_id": np.arange(W, dtype=np.int64),
         "w_arrival": now - rng.uniform(0.0, 0.4, W),
         "w_ttft": np.array([TIERS[t][0] for t in tier_w]),

@@ -37,6 +37,11 @@ CASES = [  # (name, segments, W, R, seed, flags)
     ("large_ttft_only", 2, 3000, 3000, 15, "ttft_only"),
     ("large_neither", 1, 2000, 5000, 16, "neither"),
     ("large_min_drop", 8, 2000, 3, 17, "both"),
+    # ragged batch: empty, short, exactly-32 and over-32 queues and running sets
+    # side by side (the group kernel's staged and unstaged segments in one warp)
+    ("ragged_mixed", 48, [0, 1, 5, 31, 32, 33, 40, 64, 17, 2, 32, 0] * 4,
+     [3, 0, 32, 33, 16, 1, 64, 0, 8, 40, 2, 31] * 4, 20, "both"),
+    ("ragged_long", 24, [0, 300, 33, 7, 250, 32] * 4, [60, 0, 5, 64, 32, 1] * 4, 21, "both"),
 ]
 # deadline ties (arrivals on a 2^-4 s grid, ids reversed): the LDF sort's
 # tie-breaks on every route -- warp network (<= 32), one cluster per segment
