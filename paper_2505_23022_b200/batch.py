@@ -315,6 +315,11 @@ class BatchEngine:
         torch = N.require_cuda()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
+        dev = self.device
+        if isinstance(traces, TraceTable):
+            # async copies from pinned host memory, enqueued first so that the
+            # cell packing below runs on the host while they are in flight
+            self._tr = {k: v.to(dev, non_blocking=True) for k, v in traces.host.items()}
         if isinstance(cells, np.ndarray):
             sims = cells
         else:
@@ -322,15 +327,13 @@ class BatchEngine:
         self.n_sims = len(sims)
         self.sims_host = sims
         self.mode = mode
-        dev = self.device
 
         def up(a):
             return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
-        if isinstance(traces, TraceTable):  # async copies from pinned host memory
+        if isinstance(traces, TraceTable):
             lens = traces.meta.lens
             self.trace_begin = traces.begin
-            self._tr = {k: v.to(dev, non_blocking=True) for k, v in traces.host.items()}
         else:
             lens = np.array([len(t) for t in traces], np.int64)
             begin = np.zeros(len(traces) + 1, np.int64)
