@@ -411,7 +411,13 @@ class BatchEngine:
 
     def results(self) -> np.ndarray:
         """Per-sim result rows (host, sl_result dtype); synchronizes."""
-        return self._res.cpu().numpy().view(N.RESULT_DTYPE).copy()
+        torch = self.torch
+        # through a pinned staging buffer (torch's caching host allocator): one
+        # DMA on the current stream instead of a pageable copy
+        host = torch.empty(self._res.numel(), dtype=torch.uint8, pin_memory=True)
+        host.copy_(self._res, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return host.numpy().view(N.RESULT_DTYPE).copy()
 
     def results_device(self):
         return self._res
