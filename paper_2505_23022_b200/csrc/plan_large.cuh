@@ -701,17 +701,31 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       inv = ps_result(ps);
     }
     int64_t n_run = R;
+    // software pipelined over chunks: the next chunk's fields and the slot
+    // after it are requested before this chunk's rounds (the kept list and the
+    // fields are dependent global round trips)
+    auto kslot = [&](int p) -> int32_t { return p < kept ? kept_list[p] : -1; };
+    int32_t idx_n = kslot(lane), idx_nn = kslot(32 + lane);
+    double tp_n = 1.0;
+    int32_t ln_n = 0, pd_n = 0;
+    if (idx_n >= 0) {
+      tp_n = st.w_tpot[idx_n];
+      ln_n = st.w_prompt[idx_n];
+      pd_n = st.w_pred[idx_n];
+    }
     for (int c0 = 0; c0 < kept; c0 += 32) {
       const int p = c0 + lane;
       const bool valid = p < kept;
-      int32_t idx = 0, ln = 0, pred = 0;
-      double tp = 1.0, ic = 0.0;
-      if (valid) {
-        idx = kept_list[p];
-        tp = st.w_tpot[idx];
-        ic = frcp_(tp);
-        ln = st.w_prompt[idx];
-        pred = st.w_pred[idx];
+      const int32_t idx = valid ? idx_n : 0;
+      const int32_t ln = valid ? ln_n : 0, pred = valid ? pd_n : 0;
+      const double tp = valid ? tp_n : 1.0;
+      const double ic = valid ? frcp_(tp) : 0.0;
+      idx_n = idx_nn;
+      idx_nn = kslot(c0 + 64 + lane);
+      if (idx_n >= 0) {
+        tp_n = st.w_tpot[idx_n];
+        ln_n = st.w_prompt[idx_n];
+        pd_n = st.w_pred[idx_n];
       }
       const bool solo = solo_ok(C, tp, ic, ln, pred);  // feasible alone (:279-289)
       const unsigned vmask = __ballot_sync(SL_FULL, valid);
