@@ -33,7 +33,10 @@ constexpr int kLW = 12;                    // walk warps
 constexpr int kLF = 4;                     // fold / aggregate warps
 constexpr int kLThreads = (kLW + kLF) * 32;
 constexpr int kLWalkThreads = kLW * 32;
-constexpr int kLK = 2;                     // queue items per walk thread per tile
+#ifndef SL_LK
+#define SL_LK 2
+#endif
+constexpr int kLK = SL_LK;                   // queue items per walk thread per tile
 constexpr int kLTile = kLWalkThreads * kLK;
 constexpr int kLChunks = kLK * kLW;        // warp chunks per tile
 
@@ -116,6 +119,11 @@ struct LargeSmem {
   // aggregates
   double inv_f, inv_c;  // sum(1/slo) over running: the float sum and its compensation
   double vbs_f, vbs_c;  // vbs over running with min_pre
+  // certified folds (dd_certify): the pair's double-double partials, the vbs
+  // running part as a double-double for warp 0 and whether it was certified
+  double dd_part[2][2][2];  // [inv, vbs][warp of the pair][s, c]
+  double vbs_s, vbs_cc;
+  int vbs_cert;
   double min_pre;  // min slo over running (+inf if none)
   long long lens;  // sum of current lengths over running
   double red_min[2];
@@ -330,6 +338,63 @@ __device__ __forceinline__ double div_int(int64_t a, int64_t b) {
   return b <= 128 ? div_small((double)a, (int)b) : fdiv_((double)a, (double)b);
 }
 
+// ---- certified CPython sums of positive terms.
+// CPython's sum() over floats (Neumaier: f_i = fl(f_{i-1} + x_i), the exact
+// error e_i of each add -- FastTwoSum -- chained into c by rounded adds, result
+// fl(f_n + c_n)) satisfies f_n + sum(e_i) = S exactly, and for positive terms
+// |e_i| <= u S, so |c_n - sum(e_i)| <= gamma_{n-1} n u S: f_n + c_n lies within
+// n^2 u^2 S (1 + 2nu) of the exact sum S and the result is RN(S) unless a
+// rounding midpoint of the double grid lies within that distance of S.  A
+// double-double sum (s, c) of the same terms in any order -- TwoSum per term,
+// the errors added rounded -- is within n^2 u^2 S of S as well, so with
+// T = 4 n^2 u^2 hi: if |lo| + T < half the gap from hi = RN(s + c) toward lo,
+// the sequential fold's result is hi, bit for bit.  Otherwise (probability
+// ~2^-20 n^2 u / ...: never seen) the caller runs the sequential fold.
+#ifndef SL_CERT_FOLD
+#define SL_CERT_FOLD 1  // 0: always the sequential folds (the tests build this too)
+#endif
+struct DD {
+  double s, c;
+};
+__device__ __forceinline__ void dd_add(DD& a, double x) {
+  const double t = fadd_(a.s, x);
+  const double bv = fsub_(t, a.s);
+  const double e = fadd_(fsub_(a.s, fsub_(t, bv)), fsub_(x, bv));  // exact: a.s + x - t
+  a.s = t;
+  a.c = fadd_(a.c, e);
+}
+__device__ __forceinline__ DD dd_merge(DD a, const DD& b) {
+  dd_add(a, b.s);
+  a.c = fadd_(a.c, b.c);
+  return a;
+}
+// lane 0's tree of the warp's partials, broadcast (every lane the same value)
+__device__ __forceinline__ DD dd_warp(DD a) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    DD b;
+    b.s = __shfl_down_sync(SL_FULL, a.s, o);
+    b.c = __shfl_down_sync(SL_FULL, a.c, o);
+    a = dd_merge(a, b);
+  }
+  a.s = __shfl_sync(SL_FULL, a.s, 0);
+  a.c = __shfl_sync(SL_FULL, a.c, 0);
+  return a;
+}
+__device__ __forceinline__ bool dd_certify(const DD& a, int64_t n, double* res) {
+  const double hi = fadd_(a.s, a.c);
+  const double bv = fsub_(hi, a.s);
+  const double lo = fadd_(fsub_(a.s, fsub_(hi, bv)), fsub_(a.c, bv));  // exact: a.s + a.c - hi
+  if (!(hi > 0.0) || !(hi < 1e300)) return false;
+  const double nn = (double)n;
+  const double T = fmul_(fmul_(fmul_(nn, nn), 4.930380657631324e-32), hi);  // 4 n^2 2^-106 hi
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  const double gap = lo >= 0.0 ? fsub_(nextafter(hi, kInf), hi) : fsub_(hi, nextafter(hi, 0.0));
+  if (!(fadd_(fabs(lo), T) < fmul_(gap, 0.4999))) return false;
+  *res = hi;
+  return true;
+}
+
 __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_plan_state st,
                                                                        const sl_plan_config cfg,
                                                                        sl_plan_out out) {
@@ -405,7 +470,33 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     const int f = warp - kLW;
     const double* tp = st.r_tpot + rb;
     if (f == 1 || f == 2) {  // sum(1.0 / slo) over running, in order (:121)
-      if (need_inv) {
+      bool cert = false;
+      if (need_inv && SL_CERT_FOLD) {
+        // the certified sum over both warps of the pair first (dd_certify)
+        DD a = {0.0, 0.0};
+        bool pos = true;
+        for (int j = (f - 1) * 32 + lane; j < R; j += 64) {
+          const double x = frcp_(tp[j]);
+          pos = pos && x > 0.0 && x < 1e300;
+          dd_add(a, x);
+        }
+        pos = __all_sync(SL_FULL, pos);
+        a = dd_warp(a);
+        if (lane == 0) {
+          sm.dd_part[0][f - 1][0] = pos ? a.s : -1.0;
+          sm.dd_part[0][f - 1][1] = a.c;
+        }
+        bar_sync(kBarInvPair, 64);
+        const DD a0 = {sm.dd_part[0][0][0], sm.dd_part[0][0][1]};
+        const DD a1 = {sm.dd_part[0][1][0], sm.dd_part[0][1][1]};
+        double r = 0.0;
+        cert = a0.s >= 0.0 && a1.s >= 0.0 && dd_certify(dd_merge(a0, a1), R, &r);
+        if (cert && f == 1 && lane == 0) {
+          res->inv_f = r;
+          res->inv_c = 0.0;
+        }
+      }
+      if (need_inv && !cert) {
         if (f == 1) {
           const double fs = split_fold_f(R, tp, [](double t) { return frcp_(t); }, sm.sf[0],
                                          kBarInvRing, lane);
@@ -451,16 +542,49 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     } else {
       bar_arrive(kBarAgg, agg_cnt);
     }
+    bool vcert = false;
+    if (need_vbs && SL_CERT_FOLD) {
+      // certified sum of min_pre / slo over running (the pair's 64 lanes); warp 0
+      // extends the double-double with the admitted entries and certifies the total
+      DD a = {0.0, 0.0};
+      bool pos = true;
+      for (int j = ft; j < R; j += 64) {
+        const double x = fdiv_(min_pre, tp[j]);
+        pos = pos && x > 0.0 && x < 1e300;
+        dd_add(a, x);
+      }
+      pos = __all_sync(SL_FULL, pos);
+      a = dd_warp(a);
+      if (lane == 0) {
+        sm.dd_part[1][f == 0][0] = pos ? a.s : -1.0;
+        sm.dd_part[1][f == 0][1] = a.c;
+      }
+      bar_sync(kBarRed, 64);
+      const DD a0 = {sm.dd_part[1][0][0], sm.dd_part[1][0][1]};
+      const DD a1 = {sm.dd_part[1][1][0], sm.dd_part[1][1][1]};
+      const DD t = dd_merge(a0, a1);
+      double r = 0.0;
+      vcert = a0.s >= 0.0 && a1.s >= 0.0 && dd_certify(t, R, &r);
+      if (f == 3 && lane == 0) {
+        res->vbs_s = t.s;
+        res->vbs_cc = t.c;
+        res->vbs_cert = vcert;
+      }
+    } else if (f == 3 && lane == 0) {
+      res->vbs_cert = 0;
+    }
     if (need_vbs) {  // vbs over running with the pre-admission minimum (:312-315)
-      if (f == 3) {
+      if (vcert) {
+        // certified above
+      } else if (f == 3) {
         const double fs = split_fold_f(R, tp, [&](double t) { return fdiv_(min_pre, t); },
                                        sm.sf[1], kBarVbsRing, lane);
         if (lane == 0) res->vbs_f = fs;
-        SL_LSTAMP(4);
       } else {
         const double cs = split_fold_c(R, sm.sf[1], kBarVbsRing, sm.ebuf[1], lane);
         if (lane == 0) res->vbs_c = cs;
       }
+      if (f == 3) SL_LSTAMP(4);
       if (split) {
         bar_sync(kBarVbs, vbs_cnt);
         if (f == 3 && lane == 0) flag_release(&sm.vbs_ready);
@@ -552,6 +676,23 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     for (int p = tid; p < W; p += kLWalkThreads) kept_list[p] = qidx(p);
     if (tid == 0) sm.kept = W;
   } else {
+    // software pipelined over tiles: the next tile's fields and the queue slots
+    // of the tile after it are requested before this tile's chain (each tile's
+    // gathers are two dependent round trips)
+    auto slot_of = [&](int p) -> int32_t { return p < W ? qidx(p) : -1; };
+    int32_t idx_n[kLK], idx_nn[kLK];
+    double ar_n[kLK], pf_n[kLK], tt_n[kLK];
+#pragma unroll
+    for (int k = 0; k < kLK; ++k) {
+      idx_n[k] = slot_of(k * kLWalkThreads + tid);
+      idx_nn[k] = slot_of(kLTile + k * kLWalkThreads + tid);
+      ar_n[k] = pf_n[k] = tt_n[k] = 0.0;
+      if (idx_n[k] >= 0) {
+        ar_n[k] = st.w_arrival[idx_n[k]];
+        pf_n[k] = st.w_prefill[idx_n[k]];
+        tt_n[k] = st.w_ttft[idx_n[k]];
+      }
+    }
     for (int t0 = 0; t0 < W; t0 += kLTile) {
       SL_LCLK(pt0);
       const double P0 = sm.P;
@@ -563,13 +704,16 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       for (int k = 0; k < kLK; ++k) {
         const int p = t0 + k * kLWalkThreads + tid;
         valid[k] = p < W;
-        e[k] = pf[k] = tt[k] = 0.0;
-        idx[k] = 0;
-        if (valid[k]) {
-          idx[k] = qidx(p);
-          e[k] = fsub_(now, st.w_arrival[idx[k]]);
-          pf[k] = st.w_prefill[idx[k]];
-          tt[k] = st.w_ttft[idx[k]];
+        e[k] = valid[k] ? fsub_(now, ar_n[k]) : 0.0;
+        pf[k] = valid[k] ? pf_n[k] : 0.0;
+        tt[k] = valid[k] ? tt_n[k] : 0.0;
+        idx[k] = valid[k] ? idx_n[k] : 0;
+        idx_n[k] = idx_nn[k];
+        idx_nn[k] = slot_of(t0 + 2 * kLTile + k * kLWalkThreads + tid);
+        if (idx_n[k] >= 0) {
+          ar_n[k] = st.w_arrival[idx_n[k]];
+          pf_n[k] = st.w_prefill[idx_n[k]];
+          tt_n[k] = st.w_ttft[idx_n[k]];
         }
         // fails at the tile's incoming prefix -> fails at every later one
         rej0[k] = valid[k] && !exact && fadd_(fadd_(e[k], P0), pf[k]) > tt[k];
@@ -809,23 +953,42 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       else
         bar_sync(kBarVbs, vbs_cnt);
     }
-    if (R > 0 && min_d == min_pre) {
+    const int tot = R + nadm;
+    auto slo = [&](int j) {
+      return j < tot ? (j < R ? st.r_tpot[rb + j] : st.w_tpot[adm[j - R]]) : 1.0;
+    };
+    bool done = false;
+    if (R > 0 && min_d == min_pre && sm.vbs_cert) {
+      // the running part as a certified double-double: add the admitted terms
+      // and certify the total (dd_certify), else the sequential fold below
+      DD a = {0.0, 0.0};
+      bool pos = true;
+      for (int j = R + lane; j < tot; j += 32) {
+        const double x = fdiv_(min_d, slo(j));
+        pos = pos && x > 0.0 && x < 1e300;
+        dd_add(a, x);
+      }
+      pos = __all_sync(SL_FULL, pos);
+      a = dd_warp(a);
+      const DD run = {sm.vbs_s, sm.vbs_cc};
+      done = pos && dd_certify(dd_merge(run, a), tot, &vbs);
+    }
+    if (done) {
+      j0 = tot;
+      ps_init(vs);
+    } else if (R > 0 && min_d == min_pre && !sm.vbs_cert) {
       vs = {sm.vbs_f, sm.vbs_c, 1};  // the vbs pair folded the running part with this minimum
       j0 = R;
     } else {
       ps_init(vs);
     }
-    const int tot = R + nadm;
-    auto slo = [&](int j) {
-      return j < tot ? (j < R ? st.r_tpot[rb + j] : st.w_tpot[adm[j - R]]) : 1.0;
-    };
     double t_n = slo(j0 + lane);
     for (int c0 = j0; c0 < tot; c0 += 32) {
       const double x = fdiv_(min_d, t_n);
       t_n = slo(c0 + 32 + lane);
       ps_add_warp_smem(vs, x, min(32, tot - c0), sm.fbuf);
     }
-    vbs = ps_result(vs);
+    if (!done) vbs = ps_result(vs);
   }
   if (lane == 0) {
     out.seg_counts[4 * seg + 0] = nwait;
