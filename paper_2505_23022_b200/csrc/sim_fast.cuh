@@ -253,7 +253,7 @@ __device__ __forceinline__ bool cert_scan(const Sim& s, double now, int W, int c
 #ifndef SL_WALK_MARGIN
 // relative margin of the walk's prefix bounds (2^-30); any larger value is as
 // exact (wider bounds, more chunks on the serial form): the parity tests run a
-// 2^-8 build to exercise that form (tests/test_gpu_walk_forms.py)
+// 2^-8 build to exercise that form (tests/test_gpu_variant_builds.py)
 #define SL_WALK_MARGIN 9.313225746154785e-10
 #endif
 
