@@ -338,62 +338,7 @@ __device__ __forceinline__ double div_int(int64_t a, int64_t b) {
   return b <= 128 ? div_small((double)a, (int)b) : fdiv_((double)a, (double)b);
 }
 
-// ---- certified CPython sums of positive terms.
-// CPython's sum() over floats (Neumaier: f_i = fl(f_{i-1} + x_i), the exact
-// error e_i of each add -- FastTwoSum -- chained into c by rounded adds, result
-// fl(f_n + c_n)) satisfies f_n + sum(e_i) = S exactly, and for positive terms
-// |e_i| <= u S, so |c_n - sum(e_i)| <= gamma_{n-1} n u S: f_n + c_n lies within
-// n^2 u^2 S (1 + 2nu) of the exact sum S and the result is RN(S) unless a
-// rounding midpoint of the double grid lies within that distance of S.  A
-// double-double sum (s, c) of the same terms in any order -- TwoSum per term,
-// the errors added rounded -- is within n^2 u^2 S of S as well, so with
-// T = 4 n^2 u^2 hi: if |lo| + T < half the gap from hi = RN(s + c) toward lo,
-// the sequential fold's result is hi, bit for bit.  Otherwise (probability
-// ~2^-20 n^2 u / ...: never seen) the caller runs the sequential fold.
-#ifndef SL_CERT_FOLD
-#define SL_CERT_FOLD 1  // 0: always the sequential folds (the tests build this too)
-#endif
-struct DD {
-  double s, c;
-};
-__device__ __forceinline__ void dd_add(DD& a, double x) {
-  const double t = fadd_(a.s, x);
-  const double bv = fsub_(t, a.s);
-  const double e = fadd_(fsub_(a.s, fsub_(t, bv)), fsub_(x, bv));  // exact: a.s + x - t
-  a.s = t;
-  a.c = fadd_(a.c, e);
-}
-__device__ __forceinline__ DD dd_merge(DD a, const DD& b) {
-  dd_add(a, b.s);
-  a.c = fadd_(a.c, b.c);
-  return a;
-}
-// lane 0's tree of the warp's partials, broadcast (every lane the same value)
-__device__ __forceinline__ DD dd_warp(DD a) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    DD b;
-    b.s = __shfl_down_sync(SL_FULL, a.s, o);
-    b.c = __shfl_down_sync(SL_FULL, a.c, o);
-    a = dd_merge(a, b);
-  }
-  a.s = __shfl_sync(SL_FULL, a.s, 0);
-  a.c = __shfl_sync(SL_FULL, a.c, 0);
-  return a;
-}
-__device__ __forceinline__ bool dd_certify(const DD& a, int64_t n, double* res) {
-  const double hi = fadd_(a.s, a.c);
-  const double bv = fsub_(hi, a.s);
-  const double lo = fadd_(fsub_(a.s, fsub_(hi, bv)), fsub_(a.c, bv));  // exact: a.s + a.c - hi
-  if (!(hi > 0.0) || !(hi < 1e300)) return false;
-  const double nn = (double)n;
-  const double T = fmul_(fmul_(fmul_(nn, nn), 4.930380657631324e-32), hi);  // 4 n^2 2^-106 hi
-  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  const double gap = lo >= 0.0 ? fsub_(nextafter(hi, kInf), hi) : fsub_(hi, nextafter(hi, 0.0));
-  if (!(fadd_(fabs(lo), T) < fmul_(gap, 0.4999))) return false;
-  *res = hi;
-  return true;
-}
+// certified CPython sums (DD, dd_certify): sl_device.cuh
 
 __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_plan_state st,
                                                                        const sl_plan_config cfg,
