@@ -48,6 +48,11 @@ constexpr int kBarVbs = 4;    // vbs pair (fold over running) -> warp 0
 constexpr int kBarInvRing = 5;   // 5..8: inv fold handover (full x2, empty x2)
 constexpr int kBarVbsRing = 9;   // 9..12: vbs fold handover
 constexpr int kBarInvPair = 13;  // split launch: the inv f / c warps
+constexpr int kBarPipe = 14;     // pipelined walk: warp 0 (chains) + the helper warps
+constexpr int kBarHelp = 15;     // pipelined walk: the helper warps
+#ifndef SL_WALK_PIPE
+#define SL_WALK_PIPE 1  // walk tiles staged / settled by warps 1.. under warp 0's chains
+#endif
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -108,8 +113,14 @@ struct LargeSmem {
   SplitRing sf[2];     // inv, vbs (16-byte aligned: first)
   double ebuf[2][32];  // c-chain operand broadcast buffers
   double fbuf[32];     // warp 0's fold operand buffer
-  double sv_e[kLTile], sv_pf[kLTile], sv_tt[kLTile];  // survivors of a tile, in order
-  uint8_t dec[kLTile];                                // chain decision: 1 = rejected
+  // survivors of a tile, in order, and the chain's decisions (1 = rejected); two
+  // buffers: the pipelined walk stages tile i+1 while warp 0 chains tile i
+  double sv_e[2][kLTile], sv_pf[2][kLTile], sv_tt[2][kLTile];
+  uint8_t dec[2][kLTile];
+  int32_t m_idx[2][kLTile];   // pipelined walk: each helper item's queue slot and
+  int16_t m_code[2][kLTile];  // -2 invalid, -1 rejected outright, else survivor slot
+  int n_svb[2];
+  double Pb[2];  // the prefix after each chained tile (pipelined walk)
   int cnt[2][kLChunks];
   int off[2][kLChunks];
   double P;        // walk prefix (exact, sequential)
@@ -165,11 +176,12 @@ __device__ __forceinline__ void flag_acquire(unsigned long long* bar) {
   }
 }
 
-// exclusive scan of the kLChunks counts of row r (warp 0), totals to *tot
-__device__ __forceinline__ void chunk_scan(LargeSmem& sm, int r, int lane, int* tot) {
+// exclusive scan of the nch (<= kLChunks) counts of row r (one warp), totals to *tot
+__device__ __forceinline__ void chunk_scan(LargeSmem& sm, int r, int lane, int* tot,
+                                           int nch = kLChunks) {
   static_assert(kLChunks <= 64, "two chunks per lane");
-  const int a = lane < kLChunks ? sm.cnt[r][lane] : 0;
-  const int b = lane + 32 < kLChunks ? sm.cnt[r][lane + 32] : 0;
+  const int a = lane < nch ? sm.cnt[r][lane] : 0;
+  const int b = lane + 32 < nch ? sm.cnt[r][lane + 32] : 0;
   // chunks 0..31 in lanes, then 32..63
   int x = a;
 #pragma unroll
@@ -185,8 +197,8 @@ __device__ __forceinline__ void chunk_scan(LargeSmem& sm, int r, int lane, int* 
     if (lane >= o) z += y;
   }
   const int tot_b = __shfl_sync(SL_FULL, z, 31);
-  if (lane < kLChunks) sm.off[r][lane] = x - a;
-  if (lane + 32 < kLChunks) sm.off[r][lane + 32] = tot_a + z - b;
+  if (lane < nch) sm.off[r][lane] = x - a;
+  if (lane + 32 < nch) sm.off[r][lane + 32] = tot_a + z - b;
   if (lane == 0) *tot = tot_a + tot_b;
 }
 
@@ -196,20 +208,21 @@ __device__ __forceinline__ void chunk_scan(LargeSmem& sm, int r, int lane, int* 
 // prefix -- rejected, the prefix unchanged -- and it is kept, adding its
 // prefill.  One round per kept item plus one per 64 rejected items, each a
 // lane-parallel test of a 64-item window; exact for any prefill sign.
-__device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double prefix, int lane) {
+__device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double prefix, int lane,
+                                                 int b = 0) {
   for (int base = 0; base < n; base += 64) {
     const int j0 = base + lane, j1 = base + 32 + lane;
     const bool v0 = j0 < n, v1 = j1 < n;
     double e0 = 0.0, p0 = 0.0, t0 = 0.0, e1 = 0.0, p1 = 0.0, t1 = 0.0;
     if (v0) {
-      e0 = sm.sv_e[j0];
-      p0 = sm.sv_pf[j0];
-      t0 = sm.sv_tt[j0];
+      e0 = sm.sv_e[b][j0];
+      p0 = sm.sv_pf[b][j0];
+      t0 = sm.sv_tt[b][j0];
     }
     if (v1) {
-      e1 = sm.sv_e[j1];
-      p1 = sm.sv_pf[j1];
-      t1 = sm.sv_tt[j1];
+      e1 = sm.sv_e[b][j1];
+      p1 = sm.sv_pf[b][j1];
+      t1 = sm.sv_tt[b][j1];
     }
     // the window stays in registers; each round retires the lanes up to the
     // first one that passes at the current prefix
@@ -230,8 +243,8 @@ __device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double pr
       a1 &= lane + 32 > g;
       prefix = g < 32 ? q0 : q1;
     }
-    if (v0) sm.dec[j0] = !k0;
-    if (v1) sm.dec[j1] = !k1;
+    if (v0) sm.dec[b][j0] = !k0;
+    if (v1) sm.dec[b][j1] = !k1;
   }
   return prefix;
 }
@@ -580,7 +593,7 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
         }
       }
       // chunk totals -> chunk offsets (any order, inflated below); reuse off[] as doubles
-      double* ctot = reinterpret_cast<double*>(sm.sv_e);
+      double* ctot = reinterpret_cast<double*>(sm.sv_e[0]);
 #pragma unroll
       for (int k = 0; k < kLK; ++k)
         if (lane == 31) ctot[k * kLW + warp] = v[k];
@@ -620,6 +633,144 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
   if (certified) {
     for (int p = tid; p < W; p += kLWalkThreads) kept_list[p] = qidx(p);
     if (tid == 0) sm.kept = W;
+  } else if (SL_WALK_PIPE) {
+    // Pipelined walk: warp 0 runs the exact chains tile after tile; warps 1..11
+    // ("helpers") stage tile i+1 (loads, the outright filter at a lower bound of
+    // its incoming prefix -- the prefix after tile i-1 --, survivor compaction)
+    // and settle tile i-1 (kept list, rejections) while warp 0 chains tile i.
+    // The outright filter only shortens the chain: an item failing at a lower
+    // bound of its prefix fails at the prefix, and the chain rejects the same
+    // items either way, so the decisions and their order do not depend on the
+    // bound used.
+    constexpr int kPH = kLW - 1, kPHT = kPH * 32, kPTile = kPHT * kLK, kPCh = kLK * kPH;
+    static_assert(kPTile <= kLTile && kPCh <= kLChunks, "pipelined tile fits the buffers");
+    const int ntiles = (W + kPTile - 1) / kPTile;
+    if (warp == 0) {
+      double P = 0.0;
+      for (int i = 0; i < ntiles; ++i) {
+        bar_sync(kBarPipe, kLWalkThreads);  // tile i staged; tile i-1's chain published
+        const int b = i & 1;
+        P = survivor_chain(sm, sm.n_svb[b], P, lane, b);
+        if (lane == 0) sm.Pb[b] = P;
+        __syncwarp();
+      }
+      bar_sync(kBarPipe, kLWalkThreads);  // the last chain's decisions are in
+      if (lane == 0) sm.P = P;
+    } else {
+      const int h = tid - 32, hw = warp - 1;
+      auto slot_of = [&](int p) -> int32_t { return p < W ? qidx(p) : -1; };
+      int32_t idx_n[kLK], idx_nn[kLK];
+      double ar_n[kLK], pf_n[kLK], tt_n[kLK];
+#pragma unroll
+      for (int k = 0; k < kLK; ++k) {
+        idx_n[k] = slot_of(k * kPHT + h);
+        idx_nn[k] = slot_of(kPTile + k * kPHT + h);
+        ar_n[k] = pf_n[k] = tt_n[k] = 0.0;
+        if (idx_n[k] >= 0) {
+          ar_n[k] = st.w_arrival[idx_n[k]];
+          pf_n[k] = st.w_prefill[idx_n[k]];
+          tt_n[k] = st.w_ttft[idx_n[k]];
+        }
+      }
+      // stage tile t into buffer t & 1 with outright-filter prefix P0
+      auto stage = [&](int t, double P0) {
+        const int b = t & 1, t0 = t * kPTile;
+        double e[kLK], pf[kLK], tt[kLK];
+        int32_t idx[kLK];
+        bool valid[kLK], sv[kLK];
+        int slot[kLK];
+#pragma unroll
+        for (int k = 0; k < kLK; ++k) {
+          const int p = t0 + k * kPHT + h;
+          valid[k] = p < W;
+          e[k] = valid[k] ? fsub_(now, ar_n[k]) : 0.0;
+          pf[k] = valid[k] ? pf_n[k] : 0.0;
+          tt[k] = valid[k] ? tt_n[k] : 0.0;
+          idx[k] = valid[k] ? idx_n[k] : 0;
+          idx_n[k] = idx_nn[k];
+          idx_nn[k] = slot_of(t0 + 2 * kPTile + k * kPHT + h);
+          if (idx_n[k] >= 0) {
+            ar_n[k] = st.w_arrival[idx_n[k]];
+            pf_n[k] = st.w_prefill[idx_n[k]];
+            tt_n[k] = st.w_ttft[idx_n[k]];
+          }
+          const bool rej0 = valid[k] && !exact && fadd_(fadd_(e[k], P0), pf[k]) > tt[k];
+          sv[k] = valid[k] && !rej0;
+          const unsigned m = __ballot_sync(SL_FULL, sv[k]);
+          slot[k] = __popc(m & lanemask_lt());
+          if (lane == 0) sm.cnt[0][k * kPH + hw] = __popc(m);
+          sm.m_idx[b][k * kPHT + h] = idx[k];
+          sm.m_code[b][k * kPHT + h] = (int16_t)(valid[k] ? (rej0 ? -1 : 0) : -2);
+        }
+        bar_sync(kBarHelp, kPHT);
+        if (hw == 0) chunk_scan(sm, 0, lane, &sm.n_svb[b], kPCh);
+        bar_sync(kBarHelp, kPHT);
+#pragma unroll
+        for (int k = 0; k < kLK; ++k) {
+          if (sv[k]) {
+            const int q = slot[k] + sm.off[0][k * kPH + hw];
+            sm.sv_e[b][q] = e[k];
+            sm.sv_pf[b][q] = pf[k];
+            sm.sv_tt[b][q] = tt[k];
+            sm.m_code[b][k * kPHT + h] = (int16_t)q;
+          }
+        }
+      };
+      // settle tile t (its chain's decisions are in buffer t & 1)
+      auto settle = [&](int t) {
+        const int b = t & 1;
+        bool keep[kLK], rj[kLK];
+        int kr[kLK], rr[kLK];
+        int32_t idx[kLK];
+#pragma unroll
+        for (int k = 0; k < kLK; ++k) {
+          const int c = sm.m_code[b][k * kPHT + h];
+          idx[k] = sm.m_idx[b][k * kPHT + h];
+          rj[k] = c == -1 || (c >= 0 && sm.dec[b][c]);
+          keep[k] = c != -2 && !rj[k];
+          const unsigned mk = __ballot_sync(SL_FULL, keep[k]);
+          const unsigned mr = __ballot_sync(SL_FULL, rj[k]);
+          kr[k] = __popc(mk & lanemask_lt());
+          rr[k] = __popc(mr & lanemask_lt());
+          if (lane == 0) {
+            sm.cnt[0][k * kPH + hw] = __popc(mk);
+            sm.cnt[1][k * kPH + hw] = __popc(mr);
+          }
+        }
+        bar_sync(kBarHelp, kPHT);
+        if (hw == 0) {
+          int tk, tr;
+          chunk_scan(sm, 0, lane, &tk, kPCh);
+          chunk_scan(sm, 1, lane, &tr, kPCh);
+          if (lane == 0) {
+            sm.kbase = sm.kept;
+            sm.rbase = sm.nrej;
+            sm.kept += tk;
+            sm.nrej += tr;
+          }
+        }
+        bar_sync(kBarHelp, kPHT);
+        const int kbase = sm.kbase, rbase = sm.rbase;
+#pragma unroll
+        for (int k = 0; k < kLK; ++k) {
+          if (keep[k]) kept_list[kbase + sm.off[0][k * kPH + hw] + kr[k]] = idx[k];
+          if (rj[k]) {
+            out.w_status[idx[k]] = SL_PLAN_REJECTED_TTFT;
+            out.w_pos[idx[k]] = rbase + sm.off[1][k * kPH + hw] + rr[k];
+          }
+        }
+        bar_sync(kBarHelp, kPHT);  // off / kbase are reused by the next stage / settle
+      };
+      if (ntiles > 0) stage(0, 0.0);
+      for (int i = 0; i < ntiles; ++i) {
+        bar_sync(kBarPipe, kLWalkThreads);  // tile i staged; tile i-1's chain published
+        if (i >= 1) settle(i - 1);
+        // tile i+1's outright filter at the prefix after tile i-1 (<= its own)
+        if (i + 1 < ntiles) stage(i + 1, i >= 1 ? sm.Pb[(i - 1) & 1] : 0.0);
+      }
+      bar_sync(kBarPipe, kLWalkThreads);  // the last chain's decisions are in
+      if (ntiles > 0) settle(ntiles - 1);
+    }
   } else {
     // software pipelined over tiles: the next tile's fields and the queue slots
     // of the tile after it are requested before this tile's chain (each tile's
@@ -677,9 +828,9 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       for (int k = 0; k < kLK; ++k) {
         if (sv[k]) {
           slot[k] += sm.off[0][k * kLW + warp];
-          sm.sv_e[slot[k]] = e[k];
-          sm.sv_pf[slot[k]] = pf[k];
-          sm.sv_tt[slot[k]] = tt[k];
+          sm.sv_e[0][slot[k]] = e[k];
+          sm.sv_pf[0][slot[k]] = pf[k];
+          sm.sv_tt[0][slot[k]] = tt[k];
         }
       }
       bar_sync(kBarWalk, kLWalkThreads);
@@ -707,7 +858,7 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       int kr[kLK], rr[kLK];
 #pragma unroll
       for (int k = 0; k < kLK; ++k) {
-        rj[k] = rej0[k] || (sv[k] && sm.dec[slot[k]]);
+        rj[k] = rej0[k] || (sv[k] && sm.dec[0][slot[k]]);
         keep[k] = valid[k] && !rj[k];
         const unsigned mk = __ballot_sync(SL_FULL, keep[k]);
         const unsigned mr = __ballot_sync(SL_FULL, rj[k]);
@@ -1026,6 +1177,7 @@ __device__ __forceinline__ void cluster_minmax(RadixSmem& sm, const uint64_t (&v
   cg::cluster_group cl = cg::this_cluster();
   const int cs = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
+  __syncthreads();  // every thread has read the sample's kmin / kmax (range) before
   if (threadIdx.x == 0) {
     sm.kmin = ~0ull;
     sm.kmax = 0;
