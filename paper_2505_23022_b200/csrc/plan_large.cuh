@@ -50,6 +50,9 @@ constexpr int kBarVbsRing = 9;   // 9..12: vbs fold handover
 constexpr int kBarInvPair = 13;  // split launch: the inv f / c warps
 constexpr int kBarPipe = 14;     // pipelined walk: warp 0 (chains) + the helper warps
 constexpr int kBarHelp = 15;     // pipelined walk: the helper warps
+#ifndef SL_PIPE_SOLO
+#define SL_PIPE_SOLO 1  // pipelined walk: warps 4 and 8 (warp 0's SMSP) idle (measured: 239 -> 233 us)
+#endif
 #ifndef SL_WALK_PIPE
 #define SL_WALK_PIPE 1  // walk tiles staged / settled by warps 1.. under warp 0's chains
 #endif
@@ -642,22 +645,30 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     // bound of its prefix fails at the prefix, and the chain rejects the same
     // items either way, so the decisions and their order do not depend on the
     // bound used.
-    constexpr int kPH = kLW - 1, kPHT = kPH * 32, kPTile = kPHT * kLK, kPCh = kLK * kPH;
+#if SL_PIPE_SOLO
+    // warp 0's SMSP (warps 0, 4, 8) runs the chain alone: warps 4 and 8 sit out
+    constexpr int kPH = kLW - kLW / 4;
+#else
+    constexpr int kPH = kLW - 1;
+#endif
+    constexpr int kPHT = kPH * 32, kPTile = kPHT * kLK, kPCh = kLK * kPH;
     static_assert(kPTile <= kLTile && kPCh <= kLChunks, "pipelined tile fits the buffers");
     const int ntiles = (W + kPTile - 1) / kPTile;
-    if (warp == 0) {
+    if (SL_PIPE_SOLO && warp != 0 && (warp & 3) == 0) {
+      // idle: the walk's closing barrier below
+    } else if (warp == 0) {
       double P = 0.0;
       for (int i = 0; i < ntiles; ++i) {
-        bar_sync(kBarPipe, kLWalkThreads);  // tile i staged; tile i-1's chain published
+        bar_sync(kBarPipe, 32 + kPHT);  // tile i staged; tile i-1's chain published
         const int b = i & 1;
         P = survivor_chain(sm, sm.n_svb[b], P, lane, b);
         if (lane == 0) sm.Pb[b] = P;
         __syncwarp();
       }
-      bar_sync(kBarPipe, kLWalkThreads);  // the last chain's decisions are in
+      bar_sync(kBarPipe, 32 + kPHT);  // the last chain's decisions are in
       if (lane == 0) sm.P = P;
     } else {
-      const int h = tid - 32, hw = warp - 1;
+      const int hw = SL_PIPE_SOLO ? warp - 1 - (warp >> 2) : warp - 1, h = hw * 32 + lane;
       auto slot_of = [&](int p) -> int32_t { return p < W ? qidx(p) : -1; };
       int32_t idx_n[kLK], idx_nn[kLK];
       double ar_n[kLK], pf_n[kLK], tt_n[kLK];
@@ -763,12 +774,12 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       };
       if (ntiles > 0) stage(0, 0.0);
       for (int i = 0; i < ntiles; ++i) {
-        bar_sync(kBarPipe, kLWalkThreads);  // tile i staged; tile i-1's chain published
+        bar_sync(kBarPipe, 32 + kPHT);  // tile i staged; tile i-1's chain published
         if (i >= 1) settle(i - 1);
         // tile i+1's outright filter at the prefix after tile i-1 (<= its own)
         if (i + 1 < ntiles) stage(i + 1, i >= 1 ? sm.Pb[(i - 1) & 1] : 0.0);
       }
-      bar_sync(kBarPipe, kLWalkThreads);  // the last chain's decisions are in
+      bar_sync(kBarPipe, 32 + kPHT);  // the last chain's decisions are in
       if (ntiles > 0) settle(ntiles - 1);
     }
   } else {
