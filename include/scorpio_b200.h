@@ -224,6 +224,14 @@ int sl_run_batch_launches(void);
  * costmodel.itl (simengine.py:235-237) and _admission_math (sched_scorpio.py:104). */
 int sl_selftest_div_small(const double* a, const int32_t* b, double* out, int64_t n, void* stream);
 
+/* Self-test of the certified CPython sum used by the few-large-segments folds
+ * (sum(1/slo), sched_scorpio.py:121; vbs, :312-315): for each s, the double-
+ * double sum of the positive terms x[begin[s], begin[s+1]) (device pointers)
+ * and its certificate.  out[3s] = the value CPython's sum() returns when the
+ * certificate holds, else NaN; out[3s+1], out[3s+2] = the double-double. */
+int sl_selftest_certified_sum(const double* x, const int64_t* begin, int32_t n_sums, double* out,
+                              void* stream);
+
 /* ---- batched plan_step over independent SchedulerStates ---------------
  * (sched_scorpio.plan_step, sched_scorpio.py:210-316; config 2).  A batch is S
  * "segments", each one SchedulerState (schedtypes.py:60-64): its waiting items

@@ -180,6 +180,9 @@ def lib():
     L.sl_cumulative_batch.restype = C.c_int
     L.sl_selftest_div_small.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     L.sl_selftest_div_small.restype = C.c_int
+    L.sl_selftest_certified_sum.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                            C.c_void_p]
+    L.sl_selftest_certified_sum.restype = C.c_int
     L.sl_abi_layout.argtypes = [C.POINTER(C.c_int64), C.c_int32]
     L.sl_abi_layout.restype = C.c_int
     L.sl_device_info.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_int32)]

@@ -765,6 +765,26 @@ __global__ void __launch_bounds__(128, SL_PLAN_GROUP_BLOCKS) guard_admit_group_k
   out.seg_min_fixed[my] = has_min ? slo_fixed<false>(min_d, E) : ~0ull;
 }
 
+// Self-test of the certified CPython sum (DD, dd_certify in sl_device.cuh): one
+// warp per sum of x[begin[s], begin[s+1]); out[3 s] = the certified result (NaN
+// when the certificate fails), out[3 s + 1], out[3 s + 2] = the double-double.
+__global__ void certified_sum_test_kernel(const double* __restrict__ x,
+                                          const int64_t* __restrict__ begin, int n_sums,
+                                          double* __restrict__ out) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (s >= n_sums) return;
+  DD a = {0.0, 0.0};
+  for (int64_t j = begin[s] + lane; j < begin[s + 1]; j += 32) dd_add(a, x[j]);
+  a = dd_warp(a);
+  double r = __longlong_as_double(0x7ff8000000000000LL);
+  if (!dd_certify(a, begin[s + 1] - begin[s], &r)) r = __longlong_as_double(0x7ff8000000000000LL);
+  if (lane == 0) {
+    out[3 * s] = r;
+    out[3 * s + 1] = a.s;
+    out[3 * s + 2] = a.c;
+  }
+}
+
 // ---- credit select / decode-all: one warp per segment
 __device__ __forceinline__ void seg_credit_select(const sl_plan_state& st,
                                                   const sl_plan_config& cfg,
@@ -1782,6 +1802,15 @@ int sl_plan_step_batch(const sl_plan_state* st, const sl_plan_config* cfg, int64
   if (rc) return rc;
   if (cfg->flags & SL_PLAN_GUARD_ONLY) return SL_OK;
   return sl_credit_select_batch(st, cfg, out, 1, stream);
+}
+
+int sl_selftest_certified_sum(const double* x, const int64_t* begin, int32_t n_sums, double* out,
+                              void* stream) {
+  if (n_sums < 0 || (n_sums > 0 && (!x || !begin || !out))) return SL_ERR_ARG;
+  if (n_sums == 0) return SL_OK;
+  certified_sum_test_kernel<<<(n_sums + 7) / 8, 256, 0, (cudaStream_t)stream>>>(x, begin, n_sums,
+                                                                               out);
+  return cudaGetLastError() == cudaSuccess ? SL_OK : SL_ERR_CUDA;
 }
 
 }  // extern "C"
