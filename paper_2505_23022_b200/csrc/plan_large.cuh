@@ -238,13 +238,15 @@ __device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double pr
       const unsigned ok0 = __ballot_sync(SL_FULL, a0 && !(fadd_(fadd_(e0, prefix), p0) > t0));
       const unsigned ok1 = __ballot_sync(SL_FULL, a1 && !(fadd_(fadd_(e1, prefix), p1) > t1));
       if (!(ok0 | ok1)) break;  // every remaining item fails at this prefix
-      const int g = ok0 ? __ffs(ok0) - 1 : 32 + __ffs(ok1) - 1;
-      const double q0 = __shfl_sync(SL_FULL, n0, g & 31), q1 = __shfl_sync(SL_FULL, n1, g & 31);
-      k0 |= lane == g;
-      k1 |= lane + 32 == g;
-      a0 &= lane > g;
-      a1 &= lane + 32 > g;
-      prefix = g < 32 ? q0 : q1;
+      // the first passing item: lane gl of the lower half, else of the upper;
+      // the half is chosen before the shuffle (one 64-bit shuffle on the path)
+      const bool hi = ok0 == 0;
+      const int gl = __ffs(hi ? ok1 : ok0) - 1;
+      prefix = __shfl_sync(SL_FULL, hi ? n1 : n0, gl);
+      k0 |= !hi && lane == gl;
+      k1 |= hi && lane == gl;
+      a0 &= !hi && lane > gl;
+      a1 &= !hi || lane > gl;
     }
     if (v0) sm.dec[b][j0] = !k0;
     if (v1) sm.dec[b][j1] = !k1;
