@@ -213,8 +213,11 @@ __device__ __forceinline__ void chunk_scan(LargeSmem& sm, int r, int lane, int* 
 // lane-parallel test of a 64-item window; exact for any prefill sign.
 __device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double prefix, int lane,
                                                  int b = 0) {
+  // items in reversed lane order (item t of a half in lane 31 - t): the first
+  // passing item is the highest set ballot bit (one FLO, no bit reversal)
+  const int rl = 31 - lane;
   for (int base = 0; base < n; base += 64) {
-    const int j0 = base + lane, j1 = base + 32 + lane;
+    const int j0 = base + rl, j1 = base + 32 + rl;
     const bool v0 = j0 < n, v1 = j1 < n;
     double e0 = 0.0, p0 = 0.0, t0 = 0.0, e1 = 0.0, p1 = 0.0, t1 = 0.0;
     if (v0) {
@@ -241,12 +244,12 @@ __device__ __forceinline__ double survivor_chain(LargeSmem& sm, int n, double pr
       // the first passing item: lane gl of the lower half, else of the upper;
       // the half is chosen before the shuffle (one 64-bit shuffle on the path)
       const bool hi = ok0 == 0;
-      const int gl = __ffs(hi ? ok1 : ok0) - 1;
+      const int gl = 31 - __clz(hi ? ok1 : ok0);
       prefix = __shfl_sync(SL_FULL, hi ? n1 : n0, gl);
       k0 |= !hi && lane == gl;
       k1 |= hi && lane == gl;
-      a0 &= !hi && lane > gl;
-      a1 &= !hi || lane > gl;
+      a0 &= !hi && lane < gl;  // later items of the lower half: lower lanes
+      a1 &= !hi || lane < gl;
     }
     if (v0) sm.dec[b][j0] = !k0;
     if (v1) sm.dec[b][j1] = !k1;
