@@ -53,6 +53,10 @@ constexpr int kBarHelp = 15;     // pipelined walk: the helper warps
 #ifndef SL_PIPE_SOLO
 #define SL_PIPE_SOLO 1  // pipelined walk: warps 4 and 8 (warp 0's SMSP) idle (measured: 239 -> 233 us)
 #endif
+constexpr int kAdmChunks = 1024;  // kept lists of up to 32,768 items
+#ifndef SL_ADM_PAR
+#define SL_ADM_PAR 1  // first admission round over every chunk in parallel (all walk warps)
+#endif
 #ifndef SL_WALK_PIPE
 #define SL_WALK_PIPE 1  // walk tiles staged / settled by warps 1.. under warp 0's chains
 #endif
@@ -124,6 +128,14 @@ struct LargeSmem {
   int16_t m_code[2][kLTile];  // -2 invalid, -1 rejected outright, else survivor slot
   int n_svb[2];
   double Pb[2];  // the prefix after each chained tile (pipelined walk)
+  // parallel first admission round: per 32-item chunk of the kept list, the
+  // first item passing against the pre-admission state, the failing items before
+  // it (kept waiting / rejected, as lane masks) and their output offsets
+  int a_first[kAdmChunks];
+  unsigned a_keepm[kAdmChunks], a_rejm[kAdmChunks];
+  int a_kofs[kAdmChunks], a_rofs[kAdmChunks];
+  double adm_inv;
+  int a_cstar, a_nwait, a_nrej;
   int cnt[2][kLChunks];
   int off[2][kLChunks];
   double P;        // walk prefix (exact, sequential)
@@ -935,20 +947,130 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     }
     return;
   }
+  // Parallel first admission round (all walk warps): until the first admission
+  // the state is the pre-admission one, so every chunk of the kept list is
+  // tested against it at once; the failing items before the first passing one
+  // (all of them if none passes) are settled here in queue order -- kept waiting
+  // if feasible alone, else rejected (:279-291) -- and warp 0 runs the serial
+  // rounds from the first passing item on.
+  const int nch = (kept + 31) / 32;
+  const bool apar = SL_ADM_PAR && tpot_guard && nch > 1 && nch <= kAdmChunks;
+  int c_start = 0, f_start = 0, nwait0 = 0, nrej_add = 0;
+  if (apar) {
+    if (warp == 0) {
+      if (split) {
+        flag_acquire(&sm.agg_ready);
+        flag_acquire(&sm.inv_ready);
+      } else {
+        bar_sync(kBarAgg, agg_cnt);
+      }
+      if (lane == 0) sm.adm_inv = need_inv ? ps_result(PySum{sm.inv_f, sm.inv_c, 1}) : 0.0;
+    }
+    bar_sync(kBarWalk, kLWalkThreads);
+    {
+      const double inv = sm.adm_inv, min_d = sm.min_pre;
+      const int64_t lens = sm.lens;
+      const bool has_min = R > 0;
+      for (int c = warp; c < nch; c += kLW) {
+        const int p = 32 * c + lane;
+        const bool valid = p < kept;
+        int32_t ln = 0, pred = 0;
+        double tp = 1.0, ic = 0.0;
+        if (valid) {
+          const int32_t idx = kept_list[p];
+          tp = st.w_tpot[idx];
+          ln = st.w_prompt[idx];
+          pred = st.w_pred[idx];
+          ic = frcp_(tp);
+        }
+        const bool solo = solo_ok(C, tp, ic, ln, pred);
+        const bool lt = !has_min || tp < min_d;
+        const double minp = lt ? tp : min_d;
+        const double V = fmul_(minp, fadd_(inv, ic));
+        const double L = div_int(lens + ln, (int64_t)R + 1);
+        const double est = tpot_estimate(C, V, L, pred);
+        const double thr = (r_only && has_min) ? min_d : minp;
+        const unsigned okm = __ballot_sync(SL_FULL, valid && est <= thr);
+        const int f = okm ? __ffs(okm) - 1 : 32;
+        const unsigned failm = __ballot_sync(SL_FULL, valid && lane < f);
+        const unsigned keepm = __ballot_sync(SL_FULL, valid && lane < f && solo);
+        if (lane == 0) {
+          sm.a_first[c] = f;
+          sm.a_keepm[c] = keepm;
+          sm.a_rejm[c] = failm & ~keepm;
+        }
+      }
+    }
+    bar_sync(kBarWalk, kLWalkThreads);
+    if (warp == 0) {  // the first chunk with a passing item; offsets of the settled part
+      int cstar = nch, kacc = 0, racc = 0;
+      for (int c0 = 0; c0 < nch && cstar == nch; c0 += 32) {
+        const int c = c0 + lane;
+        const bool v = c < nch;
+        const unsigned pm = __ballot_sync(SL_FULL, v && sm.a_first[c] < 32);
+        const int last = pm ? __ffs(pm) - 1 : 31;  // chunks c0 .. c0 + last settle (partly)
+        const bool in = v && lane <= last;
+        const int kc = in ? __popc(sm.a_keepm[c]) : 0, rc = in ? __popc(sm.a_rejm[c]) : 0;
+        int ks = kc, rs = rc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(SL_FULL, ks, o), z = __shfl_up_sync(SL_FULL, rs, o);
+          if (lane >= o) {
+            ks += y;
+            rs += z;
+          }
+        }
+        if (in) {
+          sm.a_kofs[c] = kacc + ks - kc;
+          sm.a_rofs[c] = racc + rs - rc;
+        }
+        kacc += __shfl_sync(SL_FULL, ks, 31);
+        racc += __shfl_sync(SL_FULL, rs, 31);
+        if (pm) cstar = c0 + __ffs(pm) - 1;
+      }
+      if (lane == 0) {
+        sm.a_cstar = cstar;
+        sm.a_nwait = kacc;
+        sm.a_nrej = racc;
+      }
+    }
+    bar_sync(kBarWalk, kLWalkThreads);
+    const int cstar = sm.a_cstar;
+    for (int c = warp; c <= min(cstar, nch - 1); c += kLW) {
+      const unsigned km = sm.a_keepm[c], rm = sm.a_rejm[c];
+      if (((km | rm) >> lane) & 1u) {
+        const int32_t idx = kept_list[32 * c + lane];
+        if ((km >> lane) & 1u) {
+          out.w_status[idx] = SL_PLAN_WAITING;
+          out.w_pos[idx] = sm.a_kofs[c] + __popc(km & lanemask_lt());
+        } else {
+          out.w_status[idx] = SL_PLAN_REJECTED_ADMISSION;
+          out.w_pos[idx] = nrej + sm.a_rofs[c] + __popc(rm & lanemask_lt());
+        }
+      }
+    }
+    c_start = cstar;
+    f_start = cstar < nch ? sm.a_first[cstar] : 0;
+    nwait0 = sm.a_nwait;
+    nrej_add = sm.a_nrej;
+  }
   if (warp != 0) return;
 
   // ---------------------------------------------------- admission (warp 0)
-  if (split) {
-    flag_acquire(&sm.agg_ready);
-    flag_acquire(&sm.inv_ready);
-  } else {
-    bar_sync(kBarAgg, agg_cnt);
+  if (!apar) {
+    if (split) {
+      flag_acquire(&sm.agg_ready);
+      flag_acquire(&sm.inv_ready);
+    } else {
+      bar_sync(kBarAgg, agg_cnt);
+    }
   }
   int64_t lens = sm.lens;
   double min_d = sm.min_pre;
   const double min_pre = min_d;
   bool has_min = R > 0;
-  int nadm = 0, nwait = 0;
+  int nadm = 0, nwait = nwait0;
+  nrej += nrej_add;
   int32_t* adm = out.adm_order + wb;
   if (tpot_guard) {
     double inv = 0.0;
@@ -961,7 +1083,8 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
     // after it are requested before this chunk's rounds (the kept list and the
     // fields are dependent global round trips)
     auto kslot = [&](int p) -> int32_t { return p < kept ? kept_list[p] : -1; };
-    int32_t idx_n = kslot(lane), idx_nn = kslot(32 + lane);
+    const int cb = 32 * c_start;  // chunks before c_start were settled in parallel
+    int32_t idx_n = kslot(cb + lane), idx_nn = kslot(cb + 32 + lane);
     double tp_n = 1.0;
     int32_t ln_n = 0, pd_n = 0;
     if (idx_n >= 0) {
@@ -969,7 +1092,7 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
       ln_n = st.w_prompt[idx_n];
       pd_n = st.w_pred[idx_n];
     }
-    for (int c0 = 0; c0 < kept; c0 += 32) {
+    for (int c0 = cb; c0 < kept; c0 += 32) {
       const int p = c0 + lane;
       const bool valid = p < kept;
       const int32_t idx = valid ? idx_n : 0;
@@ -984,7 +1107,9 @@ __global__ void __launch_bounds__(kLThreads, 1) guard_admit_cta_kernel(const sl_
         pd_n = st.w_pred[idx_n];
       }
       const bool solo = solo_ok(C, tp, ic, ln, pred);  // feasible alone (:279-289)
-      const unsigned vmask = __ballot_sync(SL_FULL, valid);
+      // (the first chunk's items before f_start were settled in parallel)
+      const unsigned vmask =
+          __ballot_sync(SL_FULL, valid) & (c0 == cb ? ~((1u << f_start) - 1u) : ~0u);
       unsigned pend = vmask, admm = 0;
       // one round per admission: every pending candidate against the same state
       while (pend) {
