@@ -47,6 +47,13 @@ CASES = [  # (name, segments, W, R, seed, flags)
 # tie-breaks on every route -- warp network (<= 32), one cluster per segment
 TIES = [("ties_small", 16, 32, 8, 18, "both", 0.0625),
         ("ties_large", 2, 5000, 50, 19, "both", 0.0625)]
+# negative prefill times (alpha_p < 0 is legal: PrefillParams checks only the
+# value at theta, costmodel.py:45-47): prompts past -beta_p/alpha_p get negative
+# prefills, so the walk's prefix can shrink -- the kernels drop their
+# prefix-monotone shortcuts (PLAN_EXACT_WALK) on every route
+NEG_PREFILL = (0.004, 128.0, -1e-5, 4.5e-3)
+NEG = [("neg_prefill_small", 32, 40, 16, 22, "both"),
+       ("neg_prefill_large", 2, 3000, 50, 23, "both")]
 # ... and 256 segments spread over the bench's 262,144-segment scaled batch
 # (config2_plan_arrays_fast, seed 11): the test runs the whole batch through the
 # same kernels the bench times and compares the sampled segments
@@ -75,12 +82,15 @@ def main() -> None:
             "ttft_only": ScorpioConfig(tpot_guard=False), "tpot_only": ScorpioConfig(ttft_guard=False),
             "neither": ScorpioConfig(False, False)}
     blobs, meta = {}, []
-    jobs = ([(name, S, W, R, seed, fl, None, None) for name, S, W, R, seed, fl in CASES]
-            + [(name, S, W, R, seed, fl, None, tg) for name, S, W, R, seed, fl, tg in TIES]
-            + [j + (None,) for j in SAMPLED])
-    for name, S, W, R, seed, fl, n_sample, tg in jobs:
+    jobs = ([(name, S, W, R, seed, fl, None, None, None) for name, S, W, R, seed, fl in CASES]
+            + [(name, S, W, R, seed, fl, None, tg, None) for name, S, W, R, seed, fl, tg in TIES]
+            + [j + (None, None) for j in SAMPLED]
+            + [(name, S, W, R, seed, fl, None, None, NEG_PREFILL)
+               for name, S, W, R, seed, fl in NEG])
+    for name, S, W, R, seed, fl, n_sample, tg, pf in jobs:
+        pre_c = PrefillParams(*pf) if pf else pre
         if n_sample is None:
-            a = config2_arrays(S, W, R, seed, tie_grid=tg)
+            a = config2_arrays(S, W, R, seed, tie_grid=tg, **({"prefill": pf} if pf else {}))
             states = states_from_arrays(a, T)
             segs = None
         else:
@@ -89,7 +99,7 @@ def main() -> None:
             states = states_from_plan_arrays(a, T, segs)
         adm, rej, bat, wait, vbs, mins, cred = [], [], [], [], [], [], []
         for st in states:
-            p = plan_step(st, pred, itl, pre, cfgs[fl])
+            p = plan_step(st, pred, itl, pre_c, cfgs[fl])
             adm.append([e.request.id for e in p.admitted])
             rej.append([w.request.id * 2 + (s.value == "rejected_admission") for w, s in p.rejected])
             bat.append([e.request.id for e in p.decode_batch])
@@ -110,7 +120,7 @@ def main() -> None:
         blobs[k + "min_slo"] = np.array(mins)
         blobs[k + "credit"] = np.array(cred, np.uint64)
         meta.append(dict(name=name, segments=S, w=W, r=R, seed=seed, flags=fl, sample=segs,
-                         tie_grid=tg))
+                         tie_grid=tg, **({"prefill": list(pf)} if pf else {})))
         print(name, "admitted", sum(map(len, adm)), "rejected", sum(map(len, rej)),
               "batch", sum(map(len, bat)))
     np.savez_compressed(os.path.join(HERE, "plan.npz"), **blobs)
