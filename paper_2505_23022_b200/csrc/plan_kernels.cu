@@ -661,6 +661,9 @@ __global__ void guard_admit_kernel(const sl_plan_state st, const sl_plan_config 
 #ifndef SL_PLAN_STAGE
 #define SL_PLAN_STAGE 1  // cp.async staging of the next segment's fields (group kernel)
 #endif
+#ifndef SL_SELECT_PF
+#define SL_SELECT_PF 1  // credit select: next segment's lines prefetched into L1
+#endif
 #ifndef SL_PLAN_GROUP_BLOCKS
 #define SL_PLAN_GROUP_BLOCKS 7  // <= 72 registers: 28 warps/SM
 #endif
@@ -839,8 +842,30 @@ __device__ __forceinline__ void seg_credit_select(const sl_plan_state& st,
 __global__ void credit_select_kernel(const sl_plan_state st, const sl_plan_config cfg,
                                      sl_plan_out out, int use_seg_min) {
   const int nw = (gridDim.x * blockDim.x) >> 5;  // grid-stride, as sort_warp_kernel
-  for (int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; seg < st.n_segments; seg += nw)
-    seg_credit_select(st, cfg, out, use_seg_min, seg, threadIdx.x & 31);
+  const int lane = threadIdx.x & 31, S = st.n_segments;
+  int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+#if SL_SELECT_PF
+  // the next segment's running lines are prefetched into L1 while this one is
+  // selected (its start loaded one segment earlier, so no prefetch waits on it)
+  int64_t bn = seg + nw < S ? st.r_begin[seg + nw] : 0;
+#endif
+  for (; seg < S; seg += nw) {
+#if SL_SELECT_PF
+    const int nx = seg + nw;
+    if (nx < S && lane < 5) {
+      const char* q = lane < 2 ? reinterpret_cast<const char*>(st.r_credit + bn) + 128 * lane
+                      : lane < 4 ? reinterpret_cast<const char*>(st.r_tpot + bn) + 128 * (lane - 2)
+                                 : reinterpret_cast<const char*>(st.r_exclude ? st.r_exclude + bn
+                                                                              : nullptr);
+      if (q) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+    }
+    const int64_t bnn = nx + nw < S ? st.r_begin[nx + nw] : 0;
+#endif
+    seg_credit_select(st, cfg, out, use_seg_min, seg, lane);
+#if SL_SELECT_PF
+    bn = bnn;
+#endif
+  }
 }
 
 // Few, large segments (the config-2 stress shape): one 1024-thread CTA per
