@@ -985,7 +985,10 @@ constexpr int kSelCtaMaxSegments = 64;
 // are pushed into every CTA's shared memory with one cluster barrier each; pass
 // 2: batch positions from the count of the slices before this one plus a
 // blocked ballot scan over the slice (the flags re-read from r_batch).
-constexpr int kSelCluster = 8;
+#ifndef SL_SEL_CLUSTER
+#define SL_SEL_CLUSTER 16  // CTAs per segment (measured at the stress shape: 4 22 us, 8 15.8 us, 16 11.5 us)
+#endif
+constexpr int kSelCluster = SL_SEL_CLUSTER;
 __device__ __forceinline__ int cta_excl_scan_i(int v, int* wtot) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int x = v;
@@ -1770,6 +1773,9 @@ int sl_credit_select_batch(const sl_plan_state* st, const sl_plan_config* cfg, s
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
+    if (kSelCluster > 8)
+      cudaFuncSetAttribute(credit_select_cluster_kernel,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (cudaLaunchKernelEx(&lc, credit_select_cluster_kernel, *st, *cfg, *out, use_seg_min) !=
         cudaSuccess)
       return SL_ERR_CUDA;
